@@ -1,0 +1,40 @@
+"""B200-native GCRO-DR-IR: mixed-precision GMRES-based iterative refinement
+with Krylov subspace recycling (arXiv 2201.09827), drop-in for the reference
+package's solver entry points (irkit.refine.solve / gmres_ir / rgmres_ir / sir).
+
+The solver path is hand-written sm_100a CUDA behind a C ABI
+(include/gcrodr_b200.h, libgcrodr_b200.so); this package is the host side.
+There is no CPU fallback.
+"""
+
+from .precision import Format, PrecisionTriple, squared_format
+from .refine import (
+    ConvergenceDecision,
+    DivergenceReason,
+    Method,
+    RefineConfig,
+    RefinementReport,
+    classify,
+    gmres_ir,
+    rgmres_ir,
+    sir,
+    solve,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Format",
+    "PrecisionTriple",
+    "squared_format",
+    "Method",
+    "DivergenceReason",
+    "RefineConfig",
+    "RefinementReport",
+    "ConvergenceDecision",
+    "classify",
+    "solve",
+    "sir",
+    "gmres_ir",
+    "rgmres_ir",
+]

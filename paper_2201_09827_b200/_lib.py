@@ -1,0 +1,243 @@
+"""ctypes binding of the C ABI in ``include/gcrodr_b200.h``.
+
+The library is the in-tree ``libgcrodr_b200.so`` built by ``_build.py``.  There
+is no CPU fallback: if the library or a GPU is missing, every solver entry
+point raises ``GpuUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgcrodr_b200.so")
+
+# formats / methods (gcrodr_b200.h)
+HALF, SINGLE, DOUBLE, QUAD = 0, 1, 2, 3
+SIR, GMRES_IR, SGMRES_IR, RGMRES_IR, RSGMRES_IR = 0, 1, 2, 3, 4
+
+ST_CONVERGED, ST_STAGNATED, ST_BREAKDOWN = 1, 2, 4
+ST_NU_ZERO, ST_NU_NONFINITE = 256, 512
+
+EXPORTS = [
+    "gb_version", "gb_last_error", "gb_device_count", "gb_solver_create", "gb_solver_destroy",
+    "gb_set_system", "gb_factorize", "gb_initial_solution", "gb_reference_solution",
+    "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
+    "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
+    "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched",
+]
+
+
+class GpuUnavailable(RuntimeError):
+    """The CUDA library or device is missing (no CPU fallback exists)."""
+
+
+class GbError(RuntimeError):
+    pass
+
+
+class Options(C.Structure):
+    _fields_ = [
+        ("uf", C.c_int), ("u", C.c_int), ("ur", C.c_int), ("method", C.c_int),
+        ("m", C.c_int), ("k", C.c_int), ("tau", C.c_double), ("max_cycles", C.c_int),
+        ("reorthogonalize", C.c_int), ("extra_precision", C.c_int), ("grid_ctas", C.c_int),
+        ("lu_mode", C.c_int),
+    ]
+
+
+class StepInfo(C.Structure):
+    _fields_ = [
+        ("nu", C.c_double), ("inner_iters", C.c_int), ("ncycles", C.c_int), ("status", C.c_int),
+        ("applies", C.c_int), ("keff", C.c_int), ("pad", C.c_int), ("ferr", C.c_double),
+        ("nbe", C.c_double), ("cbe", C.c_double),
+    ]
+
+
+class BatchOut(C.Structure):
+    _fields_ = [
+        ("converged", C.c_void_p), ("steps", C.c_void_p), ("reason", C.c_void_p),
+        ("inner", C.c_void_p), ("nbe", C.c_void_p), ("ferr", C.c_void_p), ("x", C.c_void_p),
+        ("growth", C.c_void_p), ("flags", C.c_void_p),
+    ]
+
+
+_LIB = None
+
+
+def load(path: str | None = None):
+    """Load (once) the C-ABI library; raises GpuUnavailable when absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise GpuUnavailable(f"{p} is not built (run __graft_entry__.build())")
+    lib = C.CDLL(p)
+    vp, ip, dp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double)
+    sig = {
+        "gb_version": (C.c_char_p, []),
+        "gb_last_error": (C.c_char_p, []),
+        "gb_device_count": (C.c_int, []),
+        "gb_solver_create": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(Options), vp]),
+        "gb_solver_destroy": (C.c_int, [vp]),
+        "gb_set_system": (C.c_int, [vp, vp, vp]),
+        "gb_factorize": (C.c_int, [vp, ip, dp]),
+        "gb_initial_solution": (C.c_int, [vp, ip]),
+        "gb_reference_solution": (C.c_int, [vp, ip]),
+        "gb_refine_step": (C.c_int, [vp, C.POINTER(StepInfo)]),
+        "gb_last_cycles": (C.c_int, [vp, vp, vp, C.c_int, ip]),
+        "gb_get_solution": (C.c_int, [vp, vp]),
+        "gb_get_reference": (C.c_int, [vp, vp]),
+        "gb_get_factors": (C.c_int, [vp, vp, vp]),
+        "gb_apply_preconditioned": (C.c_int, [vp, vp, vp, C.c_int]),
+        "gb_precond_rhs": (C.c_int, [vp, vp, vp, C.c_int]),
+        "gb_residual": (C.c_int, [vp, vp, vp, C.c_int]),
+        "gb_lu_solve": (C.c_int, [vp, vp, vp]),
+        "gb_last_step_ms": (C.c_double, [vp]),
+        "gb_last_factor_ms": (C.c_double, [vp]),
+        "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
+                                       vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _check(code: int, what: str) -> None:
+    if code != 0:
+        msg = _LIB.gb_last_error().decode() if _LIB is not None else "?"
+        if code == 1:
+            raise ValueError(f"{what}: {msg}")
+        if code == 2:
+            raise NotImplementedError(f"{what}: {msg}")
+        raise GbError(f"{what} failed ({code}): {msg}")
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def require_gpu():
+    lib = load()
+    if lib.gb_device_count() < 1:
+        raise GpuUnavailable("no CUDA device visible; the solver has no CPU fallback")
+    return lib
+
+
+def current_stream() -> int:
+    """torch's current CUDA stream when torch is initialised, else NULL."""
+    try:
+        import torch
+
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return int(torch.cuda.current_stream().cuda_stream)
+    except Exception:  # pragma: no cover - torch is plumbing only
+        pass
+    return 0
+
+
+class Solver:
+    """Device context for one system of order n (gb_solver)."""
+
+    def __init__(self, n: int, opts: Options, stream: int | None = None):
+        self.lib = require_gpu()
+        self.n = int(n)
+        self.opts = opts
+        h = C.c_void_p()
+        _check(self.lib.gb_solver_create(C.byref(h), self.n, C.byref(opts),
+                                         C.c_void_p(stream if stream is not None else current_stream())),
+               "gb_solver_create")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.gb_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_system(self, a: np.ndarray, b: np.ndarray) -> None:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        self._keep = (a, b)
+        _check(self.lib.gb_set_system(self.h, _ptr(a), _ptr(b)), "gb_set_system")
+
+    def factorize(self) -> tuple[int, float]:
+        z, g = C.c_int(), C.c_double()
+        _check(self.lib.gb_factorize(self.h, C.byref(z), C.byref(g)), "gb_factorize")
+        return z.value, g.value
+
+    def initial_solution(self) -> bool:
+        r = C.c_int()
+        _check(self.lib.gb_initial_solution(self.h, C.byref(r)), "gb_initial_solution")
+        return bool(r.value)
+
+    def reference_solution(self) -> bool:
+        ok = C.c_int()
+        _check(self.lib.gb_reference_solution(self.h, C.byref(ok)), "gb_reference_solution")
+        return bool(ok.value)
+
+    def step(self) -> StepInfo:
+        info = StepInfo()
+        _check(self.lib.gb_refine_step(self.h, C.byref(info)), "gb_refine_step")
+        return info
+
+    def last_cycles(self) -> tuple[list[int], list[int]]:
+        cap = self.opts.max_cycles + 1
+        it = np.zeros(cap, dtype=np.int32)
+        ke = np.zeros(cap, dtype=np.int32)
+        nc = C.c_int()
+        _check(self.lib.gb_last_cycles(self.h, _ptr(it), _ptr(ke), cap, C.byref(nc)), "gb_last_cycles")
+        return it[: nc.value].tolist(), ke[: nc.value].tolist()
+
+    def solution(self) -> np.ndarray:
+        x = np.empty(self.n)
+        _check(self.lib.gb_get_solution(self.h, _ptr(x)), "gb_get_solution")
+        return x
+
+    def reference(self) -> np.ndarray:
+        x = np.empty(self.n)
+        _check(self.lib.gb_get_reference(self.h, _ptr(x)), "gb_get_reference")
+        return x
+
+    def factors(self) -> tuple[np.ndarray, np.ndarray]:
+        lu = np.empty((self.n, self.n))
+        perm = np.empty(self.n, dtype=np.int64)
+        _check(self.lib.gb_get_factors(self.h, _ptr(lu), _ptr(perm)), "gb_get_factors")
+        return lu, perm
+
+    def _vec_op(self, fn, x, *extra) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty(self.n)
+        _check(fn(self.h, _ptr(x), _ptr(out), *extra), fn.__name__)
+        return out
+
+    def apply_preconditioned(self, v, fmt: int) -> np.ndarray:
+        return self._vec_op(self.lib.gb_apply_preconditioned, v, fmt)
+
+    def precond_rhs(self, r, fmt: int) -> np.ndarray:
+        return self._vec_op(self.lib.gb_precond_rhs, r, fmt)
+
+    def residual(self, x, fmt: int) -> np.ndarray:
+        return self._vec_op(self.lib.gb_residual, x, fmt)
+
+    def lu_solve(self, b) -> np.ndarray:
+        return self._vec_op(self.lib.gb_lu_solve, b)
+
+    @property
+    def last_step_ms(self) -> float:
+        return self.lib.gb_last_step_ms(self.h)
+
+    @property
+    def last_factor_ms(self) -> float:
+        return self.lib.gb_last_factor_ms(self.h)

@@ -1,0 +1,203 @@
+// C ABI (include/gcrodr_b200.h): argument checks, dispatch over the
+// precision variants (each compiled in its own gb_var_*.cu) and the extern "C"
+// entry points.
+#include "gb_solver.cuh"
+
+const VariantOps* gb_variant_f_h_f64() __attribute__((weak));
+const VariantOps* gb_variant_f_h_f32() __attribute__((weak));
+const VariantOps* gb_variant_f_f_f64() __attribute__((weak));
+const VariantOps* gb_variant_f_f_f32() __attribute__((weak));
+const VariantOps* gb_variant_d_h_dd() __attribute__((weak));
+const VariantOps* gb_variant_d_h_f64() __attribute__((weak));
+const VariantOps* gb_variant_d_f_dd() __attribute__((weak));
+const VariantOps* gb_variant_d_f_f64() __attribute__((weak));
+const VariantOps* gb_variant_d_d_dd() __attribute__((weak));
+const VariantOps* gb_variant_d_d_f64() __attribute__((weak));
+
+namespace {
+const VariantOps* get_variant(const VariantOps* (*fn)(), std::string& why) {
+  if (fn == nullptr) {
+    why = "precision variant not compiled into this build";
+    return nullptr;
+  }
+  return fn();
+}
+
+const VariantOps* pick_variant(const gb_options& o, std::string& why) {
+  const bool extra = o.extra_precision != 0;
+  if (o.u == GB_SINGLE) {
+    if (o.uf == GB_HALF) return get_variant(extra ? gb_variant_f_h_f64 : gb_variant_f_h_f32, why);
+    if (o.uf == GB_SINGLE) return get_variant(extra ? gb_variant_f_f_f64 : gb_variant_f_f_f32, why);
+  } else if (o.u == GB_DOUBLE) {
+    if (o.uf == GB_HALF) return get_variant(extra ? gb_variant_d_h_dd : gb_variant_d_h_f64, why);
+    if (o.uf == GB_SINGLE) return get_variant(extra ? gb_variant_d_f_dd : gb_variant_d_f_f64, why);
+    if (o.uf == GB_DOUBLE) return get_variant(extra ? gb_variant_d_d_dd : gb_variant_d_d_f64, why);
+  }
+  why = "working precision u must be single or double (u = half / quad are not built)";
+  return nullptr;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// extern "C"
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* gb_version(void) { return "gcrodr_b200 0.1 (sm_100a)"; }
+const char* gb_last_error(void) { return g_err.c_str(); }
+int gb_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+gb_status gb_solver_create(gb_solver** out, int n, const gb_options* opt, void* stream) {
+  if (!out || !opt || n < 1) return fail(GB_ERR_ARG, "bad arguments");
+  gb_options o = *opt;
+  if (!(o.m >= 1 && o.m <= n)) return fail(GB_ERR_ARG, "restart length m must satisfy 1 <= m <= n");
+  if (o.k > 32) return fail(GB_ERR_UNSUPPORTED, "recycle dimension k > 32 is not built");
+  if ((o.method == GB_RGMRES_IR || o.method == GB_RSGMRES_IR) && !(o.k >= 1 && o.k < o.m))
+    return fail(GB_ERR_ARG, "recycling methods need 1 <= k < m");
+  if (o.max_cycles < 1) return fail(GB_ERR_ARG, "max_cycles must be >= 1");
+  std::string why;
+  const VariantOps* ops = pick_variant(o, why);
+  if (!ops) return fail(GB_ERR_UNSUPPORTED, why);
+  gb_solver* s = new gb_solver();
+  s->n = n;
+  s->o = o;
+  s->stream = (cudaStream_t)stream;
+  s->ldv = (n + 31) & ~31;
+  s->lda = (n + 31) & ~31;
+  s->ops = ops;
+  if (n <= kSmallN) {
+    s->G = 1;
+  } else {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int want = o.grid_ctas > 0 ? o.grid_ctas : std::min(sms, std::max(2, (n + 127) / 128));
+    s->G = std::min(want, sms);
+  }
+  if (cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess) {
+    delete s;
+    return fail(GB_ERR_CUDA, "event create failed");
+  }
+  gb_status st = ops->setup(s);
+  if (st != GB_OK) {
+    if (s->mem) cudaFree(s->mem);
+    delete s;
+    return st;
+  }
+  *out = s;
+  return GB_OK;
+}
+
+gb_status gb_solver_destroy(gb_solver* s) {
+  if (!s) return GB_OK;
+  if (s->mem) cudaFree(s->mem);
+  if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev1) cudaEventDestroy(s->ev1);
+  delete s;
+  return GB_OK;
+}
+
+gb_status gb_set_system(gb_solver* s, const double* a, const double* b) {
+  if (!s || !a || !b) return fail(GB_ERR_ARG, "null argument");
+  gb_status st = s->ops->set_system(s, a, b);
+  if (st == GB_OK) {
+    s->have_system = true;
+    s->have_lu = s->have_x0 = false;
+  }
+  return st;
+}
+
+gb_status gb_factorize(gb_solver* s, int* zero_col, double* growth) {
+  if (!s || !s->have_system) return fail(GB_ERR_STATE, "gb_set_system first");
+  gb_status st = s->ops->factor(s, zero_col, growth);
+  if (st == GB_OK) s->have_lu = (*zero_col < 0);
+  return st;
+}
+
+gb_status gb_initial_solution(gb_solver* s, int* x0_reset) {
+  if (!s || !s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
+  gb_status st = s->ops->x0(s, x0_reset);
+  if (st == GB_OK) s->have_x0 = true;
+  return st;
+}
+
+gb_status gb_reference_solution(gb_solver* s, int* ok) {
+  if (!s || !s->have_system) return fail(GB_ERR_STATE, "gb_set_system first");
+  return s->ops->xref(s, ok);
+}
+
+gb_status gb_refine_step(gb_solver* s, gb_step_info* info) {
+  if (!s || !s->have_x0) return fail(GB_ERR_STATE, "gb_initial_solution first");
+  return s->ops->step(s, info);
+}
+
+gb_status gb_last_cycles(gb_solver* s, int* iters, int* keff, int cap, int* ncycles) {
+  if (!s) return fail(GB_ERR_ARG, "null solver");
+  int c = std::min(cap, s->o.max_cycles + 1);
+  CK(cudaMemcpyAsync(iters, s->cycle_iters, sizeof(int) * c, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(keff, s->cycle_keff, sizeof(int) * c, cudaMemcpyDeviceToHost, s->stream));
+  gb_step_info inf;
+  CK(cudaMemcpyAsync(&inf, s->out, sizeof(inf), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  *ncycles = std::min(inf.ncycles, c);
+  return GB_OK;
+}
+
+gb_status gb_get_solution(gb_solver* s, double* x) {
+  if (!s || !x) return fail(GB_ERR_ARG, "null argument");
+  return s->ops->get_x(s, x);
+}
+
+gb_status gb_get_reference(gb_solver* s, double* xref) {
+  if (!s || !xref) return fail(GB_ERR_ARG, "null argument");
+  CK(cudaMemcpyAsync(xref, s->xref, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return GB_OK;
+}
+
+gb_status gb_get_factors(gb_solver* s, double* lu, long long* perm) {
+  if (!s || !lu || !perm) return fail(GB_ERR_ARG, "null argument");
+  return s->ops->get_lu(s, lu, perm);
+}
+
+gb_status gb_apply_preconditioned(gb_solver* s, const double* v, double* w, int fmt) {
+  if (!s || !s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
+  return s->ops->debug(s, v, w, 0, fmt);
+}
+gb_status gb_precond_rhs(gb_solver* s, const double* r, double* out, int fmt) {
+  if (!s || !s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
+  return s->ops->debug(s, r, out, 1, fmt);
+}
+gb_status gb_residual(gb_solver* s, const double* x, double* r, int fmt) {
+  if (!s || !s->have_system) return fail(GB_ERR_STATE, "gb_set_system first");
+  return s->ops->debug(s, x, r, 2, fmt);
+}
+gb_status gb_lu_solve(gb_solver* s, const double* b, double* x) {
+  if (!s || !s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
+  return s->ops->debug(s, b, x, 3, s->o.uf);
+}
+
+double gb_last_step_ms(gb_solver* s) { return s ? s->last_step_ms : 0.0; }
+double gb_last_factor_ms(gb_solver* s) { return s ? s->last_factor_ms : 0.0; }
+
+gb_status gb_solve_batched(int count, int n, const gb_options* opt, int i_max, double c_conv, const double* a,
+                           const double* b, int on_device, gb_batch_out* out, double* device_ms, void* stream) {
+  (void)count;
+  (void)n;
+  (void)opt;
+  (void)i_max;
+  (void)c_conv;
+  (void)a;
+  (void)b;
+  (void)on_device;
+  (void)out;
+  (void)device_ms;
+  (void)stream;
+  return fail(GB_ERR_UNSUPPORTED, "batched mode not built yet");
+}
+
+}  // extern "C"

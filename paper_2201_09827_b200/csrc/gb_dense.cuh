@@ -1,0 +1,890 @@
+// Small dense fp64 linear algebra run by ONE CTA (the team leader): the
+// harmonic-Ritz eigenproblems, least-squares and QR of GCRO-DR
+// (reference densela.py:410-477, gcrodr.py:104-218).
+//
+// Matrices are column-major (a[i + j*ld]) fp64 in global memory.  Routines
+// named blk_* must be called by every thread of the CTA; warp_* by every
+// thread too, but only warp 0 computes (the others wait at the closing
+// __syncthreads).  Scalar bookkeeping is replicated in the participating
+// threads (identical inputs give identical values); scalar stores are done by
+// one thread followed by a barrier.
+//
+// Algorithms (restated from the published literature, not from the reference):
+//   * GEPP with first-max pivots (LAPACK dgetrf/dgetrs semantics);
+//   * Householder QR with the dlarfg sign convention + explicit Q (dgeqrf/dorgqr);
+//   * nonsymmetric eigenproblem: Householder reduction to Hessenberg form and
+//     the Francis double-shift QR iteration with accumulated Schur vectors
+//     (EISPACK orthes/hqr2), eigenvectors by back-substitution on the real
+//     Schur form for the selected eigenvalues only, normalised like LAPACK
+//     dgeev (unit 2-norm, largest component real via la_xlartg);
+//   * 2-norm condition number from a Householder bidiagonalisation and
+//     Sturm-count bisection on the Golub-Kahan tridiagonal (relative accuracy
+//     of the extreme singular values).
+#pragma once
+#include "gb_common.cuh"
+
+namespace gb {
+
+#define IX(i, j, ld) ((size_t)(i) + (size_t)(j) * (ld))
+
+constexpr double kEps53 = 1.1102230246251565e-16;  // 2^-53
+constexpr double kEps52 = 2.220446049250313e-16;   // 2^-52
+
+// ---------------------------------------------------------------------------
+// GEPP  (a: p x p in place, piv[k] = row exchanged with k) -> first zero or -1
+// ---------------------------------------------------------------------------
+static __device__ __noinline__ int blk_getrf(double* a, int ld, int p, int* piv) {
+  __shared__ int s_piv;
+  __shared__ double s_key[64];
+  __shared__ int s_idx[32];
+  int zero = -1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = 0; k < p; ++k) {
+    // first max of |a[k:, k]|
+    double bv = -1.0;
+    int bi = p;
+    for (int i = k + threadIdx.x; i < p; i += blockDim.x) {
+      double v = fabs(a[IX(i, k, ld)]);
+      if (v != v) v = __longlong_as_double(0x7ff0000000000000ull);
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_key[wid] = bv;
+      s_idx[wid] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = s_key[0];
+      int ii = s_idx[0];
+      for (int w = 1; w < nw; ++w)
+        if (s_key[w] > v || (s_key[w] == v && s_idx[w] < ii)) {
+          v = s_key[w];
+          ii = s_idx[w];
+        }
+      s_piv = ii;
+      piv[k] = ii;
+    }
+    __syncthreads();
+    const int pk = s_piv;
+    const double pv = a[IX(pk, k, ld)];
+    if (pv == 0.0) {
+      if (zero < 0) zero = k;
+      __syncthreads();
+      continue;
+    }
+    if (pk != k)
+      for (int j = threadIdx.x; j < p; j += blockDim.x) {
+        double t = a[IX(k, j, ld)];
+        a[IX(k, j, ld)] = a[IX(pk, j, ld)];
+        a[IX(pk, j, ld)] = t;
+      }
+    __syncthreads();
+    const double rp = 1.0 / pv;
+    for (int i = k + 1 + threadIdx.x; i < p; i += blockDim.x) a[IX(i, k, ld)] *= rp;
+    __syncthreads();
+    const int m = p - k - 1;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      int i = k + 1 + e % m, j = k + 1 + e / m;
+      a[IX(i, j, ld)] = __fma_rn(-a[IX(i, k, ld)], a[IX(k, j, ld)], a[IX(i, j, ld)]);
+    }
+    __syncthreads();
+  }
+  return zero;
+}
+
+// B (p x q) <- A^-1 B using blk_getrf factors; one thread per column of B.
+static __device__ __noinline__ void blk_getrs(const double* a, int ld, int p, const int* piv, double* b, int ldb,
+                                 int q) {
+  for (int c = threadIdx.x; c < q; c += blockDim.x) {
+    double* x = b + (size_t)c * ldb;
+    for (int k = 0; k < p; ++k) {
+      int pk = piv[k];
+      if (pk != k) {
+        double t = x[k];
+        x[k] = x[pk];
+        x[pk] = t;
+      }
+    }
+    for (int j = 0; j < p; ++j) {
+      double xj = x[j];
+      if (xj != 0.0)
+        for (int i = j + 1; i < p; ++i) x[i] = __fma_rn(-xj, a[IX(i, j, ld)], x[i]);
+    }
+    for (int j = p - 1; j >= 0; --j) {
+      if (x[j] != 0.0) {
+        x[j] = x[j] / a[IX(j, j, ld)];
+        double xj = x[j];
+        for (int i = 0; i < j; ++i) x[i] = __fma_rn(-xj, a[IX(i, j, ld)], x[i]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Householder QR of a (r x c, r >= c) in place: R in the upper triangle,
+// reflectors below (implicit unit), tau[c].  dlarfg convention.
+// ---------------------------------------------------------------------------
+static __device__ __noinline__ void blk_geqrf(double* a, int ld, int r, int c, double* tau) {
+  __shared__ double s_red[33];
+  __shared__ double s_beta, s_tau, s_scal;
+  for (int j = 0; j < c; ++j) {
+    double ss = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < r; i += blockDim.x) {
+      double v = a[IX(i, j, ld)];
+      ss = __fma_rn(v, v, ss);
+    }
+    double vv[1] = {ss};
+    block_sum<double, 1>(vv, s_red);
+    if (threadIdx.x == 0) {
+      double alpha = a[IX(j, j, ld)];
+      double xnorm = sqrt(vv[0]);
+      if (xnorm == 0.0) {
+        s_tau = 0.0;
+        s_beta = alpha;
+        s_scal = 1.0;
+      } else {
+        double beta = -copysign(hypot(alpha, xnorm), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_scal = 1.0 / (alpha - beta);
+        s_beta = beta;
+      }
+      tau[j] = s_tau;
+    }
+    __syncthreads();
+    const double tj = s_tau, scal = s_scal;
+    if (tj != 0.0)
+      for (int i = j + 1 + threadIdx.x; i < r; i += blockDim.x) a[IX(i, j, ld)] *= scal;
+    __syncthreads();
+    if (threadIdx.x == 0) a[IX(j, j, ld)] = s_beta;
+    // apply H_j to columns j+1..c-1: one thread per column
+    if (tj != 0.0)
+      for (int l = j + 1 + threadIdx.x; l < c; l += blockDim.x) {
+        double wv = a[IX(j, l, ld)];
+        for (int i = j + 1; i < r; ++i) wv = __fma_rn(a[IX(i, j, ld)], a[IX(i, l, ld)], wv);
+        wv *= tj;
+        a[IX(j, l, ld)] -= wv;
+        for (int i = j + 1; i < r; ++i) a[IX(i, l, ld)] = __fma_rn(-wv, a[IX(i, j, ld)], a[IX(i, l, ld)]);
+      }
+    __syncthreads();
+  }
+}
+
+// explicit Q (r x c) from blk_geqrf output (dorg2r)
+static __device__ __noinline__ void blk_orgqr(const double* a, int ld, int r, int c, const double* tau, double* q,
+                                 int ldq) {
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) {
+    int i = e % r, j = e / r;
+    q[IX(i, j, ldq)] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = c - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj != 0.0)
+      for (int l = j + threadIdx.x; l < c; l += blockDim.x) {
+        double wv = q[IX(j, l, ldq)];
+        for (int i = j + 1; i < r; ++i) wv = __fma_rn(a[IX(i, j, ld)], q[IX(i, l, ldq)], wv);
+        wv *= tj;
+        q[IX(j, l, ldq)] -= wv;
+        for (int i = j + 1; i < r; ++i) q[IX(i, l, ldq)] = __fma_rn(-wv, a[IX(i, j, ld)], q[IX(i, l, ldq)]);
+      }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// qr_reduced (densela.py:410-432): Q, R with diag(R) >= 0; returns false when
+// rank deficient (|R_ii| < max(r,c) * 2^-53 * ||R||_F) or non-finite.
+// `a` is destroyed; q (r x c, ldq), rr (c x c, ldr).
+// ---------------------------------------------------------------------------
+static __device__ __noinline__ bool blk_qr_signed(double* a, int ld, int r, int c, double* q, int ldq, double* rr,
+                                     int ldr, double* tau) {
+  __shared__ int s_bad;
+  __shared__ double s_red[33];
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) {
+    double v = a[IX(e % r, e / r, ld)];
+    if (!isfinite(v)) s_bad = 1;
+  }
+  __syncthreads();
+  if (s_bad) return false;
+  blk_geqrf(a, ld, r, c, tau);
+  blk_orgqr(a, ld, r, c, tau, q, ldq);
+  // sign fix and Frobenius norm
+  double fro = 0.0;
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
+    int i = e % c, j = e / c;
+    double v = (i <= j) ? a[IX(i, j, ld)] : 0.0;
+    double s = a[IX(i, i, ld)] < 0.0 ? -1.0 : 1.0;
+    rr[IX(i, j, ldr)] = v * s;
+    fro = __fma_rn(v, v, fro);
+  }
+  double ff[1] = {fro};
+  block_sum<double, 1>(ff, s_red);
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) {
+    int j = e / r;
+    if (a[IX(j, j, ld)] < 0.0) q[IX(e % r, j, ldq)] = -q[IX(e % r, j, ldq)];
+  }
+  __syncthreads();
+  const double tol = (double)max(r, c) * kEps53 * sqrt(ff[0]);
+  bool ok = true;
+  for (int i = 0; i < c; ++i)
+    if (fabs(rr[IX(i, i, ldr)]) < tol) ok = false;
+  __syncthreads();
+  return ok;
+}
+
+// y = R^-1 g for upper-triangular R (c x c, ld), zero-diagonal entries give 0
+// (the reference falls back to lstsq there; gmres.py:117-120).
+static __device__ __noinline__ void blk_upper_solve(const double* rmat, int ld, int c, const double* g, double* y) {
+  if (threadIdx.x == 0) {
+    for (int i = c - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int j = i + 1; j < c; ++j) s = __fma_rn(-rmat[IX(i, j, ld)], y[j], s);
+      double d = rmat[IX(i, i, ld)];
+      y[i] = d != 0.0 ? s / d : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// least squares min ||G y - rhs|| via Householder QR (gcrodr.py:212-218).
+// g (r x c) destroyed.  y[c].
+static __device__ __noinline__ void blk_lstsq(double* g, int ld, int r, int c, const double* rhs, double* y,
+                                 double* tau, double* tmp) {
+  blk_geqrf(g, ld, r, c, tau);
+  // tmp = Q^T rhs (apply reflectors in order)
+  for (int i = threadIdx.x; i < r; i += blockDim.x) tmp[i] = rhs[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < c; ++j) {
+      double tj = tau[j];
+      if (tj == 0.0) continue;
+      double wv = tmp[j];
+      for (int i = j + 1; i < r; ++i) wv = __fma_rn(g[IX(i, j, ld)], tmp[i], wv);
+      wv *= tj;
+      tmp[j] -= wv;
+      for (int i = j + 1; i < r; ++i) tmp[i] = __fma_rn(-wv, g[IX(i, j, ld)], tmp[i]);
+    }
+  }
+  __syncthreads();
+  blk_upper_solve(g, ld, c, tmp, y);
+}
+
+// ---------------------------------------------------------------------------
+// 2-norm condition number (np.linalg.cond): sigma_max / sigma_min
+// b (p x p) destroyed.
+// ---------------------------------------------------------------------------
+__device__ inline double tgk_count(const double* bd, int len, double x) {
+  // eigenvalues < x of the zero-diagonal tridiagonal with off-diagonal bd
+  const double pivmin = 1e-300;
+  double q = -x;
+  int cnt = q < 0.0;
+  for (int t = 0; t < len; ++t) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = -x - (bd[t] * bd[t]) / q;
+    cnt += q < 0.0;
+  }
+  return (double)cnt;
+}
+
+static __device__ __noinline__ double blk_cond2(double* b, int ld, int p, double* bd /* 2p */, double* tmp) {
+  __shared__ double s_red[33];
+  __shared__ double s_tau, s_beta, s_scal;
+  if (p == 1) {
+    double v = fabs(b[0]);
+    return v == 0.0 ? INFINITY : 1.0;
+  }
+  // Golub-Kahan bidiagonalisation
+  for (int i = 0; i < p; ++i) {
+    // left reflector on column i, rows i..p-1
+    double ss = 0.0;
+    for (int r = i + 1 + threadIdx.x; r < p; r += blockDim.x) ss = __fma_rn(b[IX(r, i, ld)], b[IX(r, i, ld)], ss);
+    double vv[1] = {ss};
+    block_sum<double, 1>(vv, s_red);
+    if (threadIdx.x == 0) {
+      double alpha = b[IX(i, i, ld)], xn = sqrt(vv[0]);
+      if (xn == 0.0) {
+        s_tau = 0.0;
+        s_beta = alpha;
+        s_scal = 1.0;
+      } else {
+        double beta = -copysign(hypot(alpha, xn), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_scal = 1.0 / (alpha - beta);
+        s_beta = beta;
+      }
+    }
+    __syncthreads();
+    double tj = s_tau;
+    if (tj != 0.0) {
+      for (int r = i + 1 + threadIdx.x; r < p; r += blockDim.x) b[IX(r, i, ld)] *= s_scal;
+      __syncthreads();
+      for (int l = i + 1 + threadIdx.x; l < p; l += blockDim.x) {
+        double wv = b[IX(i, l, ld)];
+        for (int r = i + 1; r < p; ++r) wv = __fma_rn(b[IX(r, i, ld)], b[IX(r, l, ld)], wv);
+        wv *= tj;
+        b[IX(i, l, ld)] -= wv;
+        for (int r = i + 1; r < p; ++r) b[IX(r, l, ld)] = __fma_rn(-wv, b[IX(r, i, ld)], b[IX(r, l, ld)]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) bd[2 * i] = s_beta;
+    __syncthreads();
+    if (i >= p - 1) break;
+    // right reflector on row i, columns i+1..p-1
+    ss = 0.0;
+    for (int c = i + 2 + threadIdx.x; c < p; c += blockDim.x) ss = __fma_rn(b[IX(i, c, ld)], b[IX(i, c, ld)], ss);
+    vv[0] = ss;
+    block_sum<double, 1>(vv, s_red);
+    if (threadIdx.x == 0) {
+      double alpha = b[IX(i, i + 1, ld)], xn = sqrt(vv[0]);
+      if (xn == 0.0) {
+        s_tau = 0.0;
+        s_beta = alpha;
+        s_scal = 1.0;
+      } else {
+        double beta = -copysign(hypot(alpha, xn), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_scal = 1.0 / (alpha - beta);
+        s_beta = beta;
+      }
+    }
+    __syncthreads();
+    tj = s_tau;
+    if (tj != 0.0) {
+      for (int c = i + 2 + threadIdx.x; c < p; c += blockDim.x) b[IX(i, c, ld)] *= s_scal;
+      __syncthreads();
+      for (int r = i + 1 + threadIdx.x; r < p; r += blockDim.x) {
+        double wv = b[IX(r, i + 1, ld)];
+        for (int c = i + 2; c < p; ++c) wv = __fma_rn(b[IX(i, c, ld)], b[IX(r, c, ld)], wv);
+        wv *= tj;
+        b[IX(r, i + 1, ld)] -= wv;
+        for (int c = i + 2; c < p; ++c) b[IX(r, c, ld)] = __fma_rn(-wv, b[IX(i, c, ld)], b[IX(r, c, ld)]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) bd[2 * i + 1] = s_beta;
+    __syncthreads();
+  }
+  __shared__ double s_res[2];
+  const int len = 2 * p - 1;
+  if (threadIdx.x < 2) {
+    // bound on the spectrum
+    double bnd = 0.0;
+    for (int t = 0; t < len; ++t) {
+      double l = t > 0 ? fabs(bd[t - 1]) : 0.0;
+      bnd = fmax(bnd, l + fabs(bd[t]));
+    }
+    bnd = fmax(bnd, fabs(bd[len - 1]));
+    bnd = bnd * (1.0 + 4.0 * kEps52) + 1e-300;
+    // bisection on the ordered bit patterns of positive doubles
+    const double target = threadIdx.x == 0 ? (double)(2 * p) : (double)(p + 1);
+    unsigned long long lo = 0ull, hi = (unsigned long long)__double_as_longlong(bnd);
+    if (threadIdx.x == 0) {
+      // largest: smallest x with count(x) >= 2p
+      while (hi - lo > 1) {
+        unsigned long long mid = lo + (hi - lo) / 2;
+        if (tgk_count(bd, len, __longlong_as_double((long long)mid)) >= target) hi = mid;
+        else lo = mid;
+      }
+    } else {
+      if (tgk_count(bd, len, __longlong_as_double(1ll)) >= target) {
+        hi = 0ull;  // exactly singular
+      } else {
+        while (hi - lo > 1) {
+          unsigned long long mid = lo + (hi - lo) / 2;
+          if (tgk_count(bd, len, __longlong_as_double((long long)mid)) >= target) hi = mid;
+          else lo = mid;
+        }
+      }
+    }
+    s_res[threadIdx.x] = __longlong_as_double((long long)hi);
+  }
+  __syncthreads();
+  double smax = s_res[0], smin = s_res[1];
+  __syncthreads();
+  (void)tmp;
+  return smin == 0.0 ? INFINITY : smax / smin;
+}
+
+// ---------------------------------------------------------------------------
+// nonsymmetric eigenproblem (warp 0).  h (p x p) in, overwritten by the real
+// Schur form T; z (p x p) Schur vectors; wr, wi eigenvalues in Schur order.
+// Returns false on non-convergence.
+// ---------------------------------------------------------------------------
+static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
+                                double* ort) {
+  const int lane = threadIdx.x & 31;
+  const int nn = p, low = 0, high = p - 1;
+  // --- orthes: Householder reduction to Hessenberg form ---
+  for (int m = low + 1; m <= high - 1; ++m) {
+    double scale = 0.0;
+    for (int i = m + lane; i <= high; i += 32) scale += fabs(H[IX(i, m - 1, ld)]);
+    scale = warp_sum(scale);
+    if (scale == 0.0) continue;
+    double hh = 0.0;
+    for (int i = m + lane; i <= high; i += 32) {
+      double o = H[IX(i, m - 1, ld)] / scale;
+      ort[i] = o;
+      hh = __fma_rn(o, o, hh);
+    }
+    hh = warp_sum(hh);
+    __syncwarp();
+    double om = ort[m];
+    double g = sqrt(hh);
+    if (om > 0) g = -g;
+    hh = hh - om * g;
+    __syncwarp();
+    if (lane == 0) ort[m] = om - g;
+    __syncwarp();
+    for (int j = m + lane; j < nn; j += 32) {
+      double f = 0.0;
+      for (int i = high; i >= m; --i) f = __fma_rn(ort[i], H[IX(i, j, ld)], f);
+      f = f / hh;
+      for (int i = m; i <= high; ++i) H[IX(i, j, ld)] = __fma_rn(-f, ort[i], H[IX(i, j, ld)]);
+    }
+    __syncwarp();
+    for (int i = lane; i <= high; i += 32) {
+      double f = 0.0;
+      for (int j = high; j >= m; --j) f = __fma_rn(ort[j], H[IX(i, j, ld)], f);
+      f = f / hh;
+      for (int j = m; j <= high; ++j) H[IX(i, j, ld)] = __fma_rn(-f, ort[j], H[IX(i, j, ld)]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      ort[m] = scale * ort[m];
+      H[IX(m, m - 1, ld)] = scale * g;
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < nn * nn; e += 32) Z[IX(e % nn, e / nn, ldz)] = (e % nn == e / nn) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int m = high - 1; m >= low + 1; --m) {
+    double hm = H[IX(m, m - 1, ld)];
+    if (hm == 0.0) continue;
+    for (int i = m + 1 + lane; i <= high; i += 32) ort[i] = H[IX(i, m - 1, ld)];
+    __syncwarp();
+    for (int j = m + lane; j <= high; j += 32) {
+      double g = 0.0;
+      for (int i = m; i <= high; ++i) g = __fma_rn(ort[i], Z[IX(i, j, ldz)], g);
+      g = (g / ort[m]) / hm;
+      for (int i = m; i <= high; ++i) Z[IX(i, j, ldz)] = __fma_rn(g, ort[i], Z[IX(i, j, ldz)]);
+    }
+    __syncwarp();
+  }
+  // clear below the subdiagonal
+  for (int e = lane; e < nn * nn; e += 32) {
+    int i = e % nn, j = e / nn;
+    if (i > j + 1) H[IX(i, j, ld)] = 0.0;
+  }
+  __syncwarp();
+
+  // --- hqr2: Francis double-shift QR with accumulation ---
+  int n = nn - 1;
+  const double eps = kEps52;
+  double exshift = 0.0, p_ = 0, q = 0, r = 0, s = 0, z = 0, t, w, x, y;
+  double norm = 0.0;
+  for (int i = lane; i < nn; i += 32)
+    for (int j = max(i - 1, 0); j < nn; ++j) norm += fabs(H[IX(i, j, ld)]);
+  norm = warp_sum(norm);
+  int iter = 0, total = 0;
+  const int itmax = 40 * max(10, nn);
+  while (n >= low) {
+    int l = n;
+    while (l > low) {
+      s = fabs(H[IX(l - 1, l - 1, ld)]) + fabs(H[IX(l, l, ld)]);
+      if (s == 0.0) s = norm;
+      if (fabs(H[IX(l, l - 1, ld)]) < eps * s) break;
+      l--;
+    }
+    if (l == n) {
+      __syncwarp();
+      if (lane == 0) {
+        H[IX(n, n, ld)] = H[IX(n, n, ld)] + exshift;
+        wr[n] = H[IX(n, n, ld)];
+        wi[n] = 0.0;
+      }
+      __syncwarp();
+      n--;
+      iter = 0;
+    } else if (l == n - 1) {
+      w = H[IX(n, n - 1, ld)] * H[IX(n - 1, n, ld)];
+      p_ = (H[IX(n - 1, n - 1, ld)] - H[IX(n, n, ld)]) / 2.0;
+      q = p_ * p_ + w;
+      z = sqrt(fabs(q));
+      double hnn = H[IX(n, n, ld)] + exshift;
+      double hn1 = H[IX(n - 1, n - 1, ld)] + exshift;
+      __syncwarp();
+      if (lane == 0) {
+        H[IX(n, n, ld)] = hnn;
+        H[IX(n - 1, n - 1, ld)] = hn1;
+      }
+      __syncwarp();
+      x = hnn;
+      if (q >= 0) {
+        z = (p_ >= 0) ? p_ + z : p_ - z;
+        double d1 = x + z, d2 = d1;
+        if (z != 0.0) d2 = x - w / z;
+        if (lane == 0) {
+          wr[n - 1] = d1;
+          wr[n] = d2;
+          wi[n - 1] = 0.0;
+          wi[n] = 0.0;
+        }
+        x = H[IX(n, n - 1, ld)];
+        s = fabs(x) + fabs(z);
+        p_ = x / s;
+        q = z / s;
+        r = sqrt(p_ * p_ + q * q);
+        p_ = p_ / r;
+        q = q / r;
+        __syncwarp();
+        for (int j = n - 1 + lane; j < nn; j += 32) {
+          double zz = H[IX(n - 1, j, ld)];
+          H[IX(n - 1, j, ld)] = q * zz + p_ * H[IX(n, j, ld)];
+          H[IX(n, j, ld)] = q * H[IX(n, j, ld)] - p_ * zz;
+        }
+        __syncwarp();
+        for (int i = lane; i <= n; i += 32) {
+          double zz = H[IX(i, n - 1, ld)];
+          H[IX(i, n - 1, ld)] = q * zz + p_ * H[IX(i, n, ld)];
+          H[IX(i, n, ld)] = q * H[IX(i, n, ld)] - p_ * zz;
+        }
+        for (int i = low + lane; i <= high; i += 32) {
+          double zz = Z[IX(i, n - 1, ldz)];
+          Z[IX(i, n - 1, ldz)] = q * zz + p_ * Z[IX(i, n, ldz)];
+          Z[IX(i, n, ldz)] = q * Z[IX(i, n, ldz)] - p_ * zz;
+        }
+        __syncwarp();
+      } else {
+        if (lane == 0) {
+          wr[n - 1] = x + p_;
+          wr[n] = x + p_;
+          wi[n - 1] = z;
+          wi[n] = -z;
+        }
+        __syncwarp();
+      }
+      n = n - 2;
+      iter = 0;
+    } else {
+      x = H[IX(n, n, ld)];
+      y = 0.0;
+      w = 0.0;
+      if (l < n) {
+        y = H[IX(n - 1, n - 1, ld)];
+        w = H[IX(n, n - 1, ld)] * H[IX(n - 1, n, ld)];
+      }
+      if (iter == 10) {
+        exshift += x;
+        __syncwarp();
+        for (int i = low + lane; i <= n; i += 32) H[IX(i, i, ld)] -= x;
+        __syncwarp();
+        s = fabs(H[IX(n, n - 1, ld)]) + fabs(H[IX(n - 1, n - 2, ld)]);
+        x = y = 0.75 * s;
+        w = -0.4375 * s * s;
+      }
+      if (iter == 30) {
+        s = (y - x) / 2.0;
+        s = s * s + w;
+        if (s > 0) {
+          s = sqrt(s);
+          if (y < x) s = -s;
+          s = x - w / ((y - x) / 2.0 + s);
+          __syncwarp();
+          for (int i = low + lane; i <= n; i += 32) H[IX(i, i, ld)] -= s;
+          __syncwarp();
+          exshift += s;
+          x = y = w = 0.964;
+        }
+      }
+      iter++;
+      if (++total > itmax) return false;
+      int m = n - 2;
+      while (m >= l) {
+        z = H[IX(m, m, ld)];
+        r = x - z;
+        s = y - z;
+        p_ = (r * s - w) / H[IX(m + 1, m, ld)] + H[IX(m, m + 1, ld)];
+        q = H[IX(m + 1, m + 1, ld)] - z - r - s;
+        r = H[IX(m + 2, m + 1, ld)];
+        s = fabs(p_) + fabs(q) + fabs(r);
+        p_ = p_ / s;
+        q = q / s;
+        r = r / s;
+        if (m == l) break;
+        if (fabs(H[IX(m, m - 1, ld)]) * (fabs(q) + fabs(r)) <
+            eps * (fabs(p_) * (fabs(H[IX(m - 1, m - 1, ld)]) + fabs(z) + fabs(H[IX(m + 1, m + 1, ld)]))))
+          break;
+        m--;
+      }
+      __syncwarp();
+      for (int i = m + 2 + lane; i <= n; i += 32) {
+        H[IX(i, i - 2, ld)] = 0.0;
+        if (i > m + 2) H[IX(i, i - 3, ld)] = 0.0;
+      }
+      __syncwarp();
+      for (int k = m; k <= n - 1; ++k) {
+        bool notlast = (k != n - 1);
+        if (k != m) {
+          p_ = H[IX(k, k - 1, ld)];
+          q = H[IX(k + 1, k - 1, ld)];
+          r = notlast ? H[IX(k + 2, k - 1, ld)] : 0.0;
+          x = fabs(p_) + fabs(q) + fabs(r);
+          if (x == 0.0) continue;
+          p_ = p_ / x;
+          q = q / x;
+          r = r / x;
+        }
+        s = sqrt(p_ * p_ + q * q + r * r);
+        if (p_ < 0) s = -s;
+        if (s != 0) {
+          __syncwarp();
+          if (lane == 0) {
+            if (k != m) H[IX(k, k - 1, ld)] = -s * x;
+            else if (l != m) H[IX(k, k - 1, ld)] = -H[IX(k, k - 1, ld)];
+          }
+          __syncwarp();
+          p_ = p_ + s;
+          x = p_ / s;
+          y = q / s;
+          z = r / s;
+          q = q / p_;
+          r = r / p_;
+          for (int j = k + lane; j < nn; j += 32) {
+            double pp = H[IX(k, j, ld)] + q * H[IX(k + 1, j, ld)];
+            if (notlast) {
+              pp = pp + r * H[IX(k + 2, j, ld)];
+              H[IX(k + 2, j, ld)] = H[IX(k + 2, j, ld)] - pp * z;
+            }
+            H[IX(k, j, ld)] = H[IX(k, j, ld)] - pp * x;
+            H[IX(k + 1, j, ld)] = H[IX(k + 1, j, ld)] - pp * y;
+          }
+          __syncwarp();
+          const int iend = min(n, k + 3);
+          for (int i = lane; i <= iend; i += 32) {
+            double pp = x * H[IX(i, k, ld)] + y * H[IX(i, k + 1, ld)];
+            if (notlast) {
+              pp = pp + z * H[IX(i, k + 2, ld)];
+              H[IX(i, k + 2, ld)] = H[IX(i, k + 2, ld)] - pp * r;
+            }
+            H[IX(i, k, ld)] = H[IX(i, k, ld)] - pp;
+            H[IX(i, k + 1, ld)] = H[IX(i, k + 1, ld)] - pp * q;
+          }
+          for (int i = low + lane; i <= high; i += 32) {
+            double pp = x * Z[IX(i, k, ldz)] + y * Z[IX(i, k + 1, ldz)];
+            if (notlast) {
+              pp = pp + z * Z[IX(i, k + 2, ldz)];
+              Z[IX(i, k + 2, ldz)] = Z[IX(i, k + 2, ldz)] - pp * r;
+            }
+            Z[IX(i, k, ldz)] = Z[IX(i, k, ldz)] - pp;
+            Z[IX(i, k + 1, ldz)] = Z[IX(i, k + 1, ldz)] - pp * q;
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+GB_DEVICE void cdiv(double xr, double xi, double yr, double yi, double& cr, double& ci) {
+  double rr, d;
+  if (fabs(yr) > fabs(yi)) {
+    rr = yi / yr;
+    d = yr + rr * yi;
+    cr = (xr + rr * xi) / d;
+    ci = (xi - rr * xr) / d;
+  } else {
+    rr = yr / yi;
+    d = yi + rr * yr;
+    cr = (rr * xr + xi) / d;
+    ci = (rr * xi - xr) / d;
+  }
+}
+
+// Eigenvector(s) for Schur position `col` (real: one vector; complex pair
+// (col, col+1) with wi[col] > 0: re/im), computed by ONE thread.  T is the
+// final quasi-triangular matrix, X a p x 2 scratch (ldx), out_re/out_im length
+// p vectors in the original basis (Z X), normalised like LAPACK dgeev.
+static __device__ __noinline__ void eigvec_one(const double* T, int ld, int p, const double* Z, int ldz,
+                                  const double* wr, const double* wi, double normT, int col, double* X,
+                                  int ldx, double* out_re, double* out_im) {
+  const double eps = kEps52;
+  const bool cplx = wi[col] != 0.0;
+  double* xr = X;        // column n-1 (real part) for complex, the vector for real
+  double* xi = X + ldx;  // column n   (imag part)
+  if (!cplx) {
+    const int n = col;
+    const double pp = wr[n];
+    for (int i = 0; i < p; ++i) xr[i] = 0.0;
+    xr[n] = 1.0;
+    int l = n;
+    double z = 0, s = 0;
+    for (int i = n - 1; i >= 0; --i) {
+      double w = T[IX(i, i, ld)] - pp;
+      double r = 0.0;
+      for (int j = l; j <= n; ++j) r += T[IX(i, j, ld)] * xr[j];
+      if (wi[i] < 0.0) {
+        z = w;
+        s = r;
+      } else {
+        l = i;
+        if (wi[i] == 0.0) {
+          xr[i] = (w != 0.0) ? -r / w : -r / (eps * normT);
+        } else {
+          double x = T[IX(i, i + 1, ld)], y = T[IX(i + 1, i, ld)];
+          double q = (wr[i] - pp) * (wr[i] - pp) + wi[i] * wi[i];
+          double t = (x * s - z * r) / q;
+          xr[i] = t;
+          xr[i + 1] = (fabs(x) > fabs(z)) ? (-r - w * t) / x : (-s - y * t) / z;
+        }
+        double t = fabs(xr[i]);
+        if ((eps * t) * t > 1)
+          for (int j = i; j <= n; ++j) xr[j] /= t;
+      }
+    }
+    // back-transform and normalise
+    double nrm = 0.0;
+    for (int i = 0; i < p; ++i) {
+      double v = 0.0;
+      for (int k = 0; k <= n; ++k) v += Z[IX(i, k, ldz)] * xr[k];
+      out_re[i] = v;
+      nrm += v * v;
+    }
+    nrm = sqrt(nrm);
+    double inv = nrm > 0 ? 1.0 / nrm : 1.0;
+    for (int i = 0; i < p; ++i) {
+      out_re[i] *= inv;
+      out_im[i] = 0.0;
+    }
+    return;
+  }
+  // complex pair: Schur positions (col, col+1), wi[col] > 0; hqr2 builds it at n = col+1
+  const int n = col + 1;
+  const double pp = wr[n], q = wi[n];  // q < 0
+  for (int i = 0; i < p; ++i) {
+    xr[i] = 0.0;
+    xi[i] = 0.0;
+  }
+  int l = n - 1;
+  if (fabs(T[IX(n, n - 1, ld)]) > fabs(T[IX(n - 1, n, ld)])) {
+    xr[n - 1] = q / T[IX(n, n - 1, ld)];
+    xi[n - 1] = -(T[IX(n, n, ld)] - pp) / T[IX(n, n - 1, ld)];
+  } else {
+    double cr, ci;
+    cdiv(0.0, -T[IX(n - 1, n, ld)], T[IX(n - 1, n - 1, ld)] - pp, q, cr, ci);
+    xr[n - 1] = cr;
+    xi[n - 1] = ci;
+  }
+  xr[n] = 0.0;
+  xi[n] = 1.0;
+  double z = 0, r = 0, s = 0;
+  for (int i = n - 2; i >= 0; --i) {
+    double ra = 0.0, sa = 0.0;
+    for (int j = l; j <= n; ++j) {
+      ra += T[IX(i, j, ld)] * xr[j];
+      sa += T[IX(i, j, ld)] * xi[j];
+    }
+    double w = T[IX(i, i, ld)] - pp;
+    if (wi[i] < 0.0) {
+      z = w;
+      r = ra;
+      s = sa;
+    } else {
+      l = i;
+      if (wi[i] == 0.0) {
+        double cr, ci;
+        cdiv(-ra, -sa, w, q, cr, ci);
+        xr[i] = cr;
+        xi[i] = ci;
+      } else {
+        double x = T[IX(i, i + 1, ld)], y = T[IX(i + 1, i, ld)];
+        double vr = (wr[i] - pp) * (wr[i] - pp) + wi[i] * wi[i] - q * q;
+        double vi = (wr[i] - pp) * 2.0 * q;
+        if (vr == 0.0 && vi == 0.0)
+          vr = eps * normT * (fabs(w) + fabs(q) + fabs(x) + fabs(y) + fabs(z));
+        double cr, ci;
+        cdiv(x * r - z * ra + q * sa, x * s - z * sa - q * ra, vr, vi, cr, ci);
+        xr[i] = cr;
+        xi[i] = ci;
+        if (fabs(x) > (fabs(z) + fabs(q))) {
+          xr[i + 1] = (-ra - w * xr[i] + q * xi[i]) / x;
+          xi[i + 1] = (-sa - w * xi[i] - q * xr[i]) / x;
+        } else {
+          cdiv(-r - y * xr[i], -s - y * xi[i], z, q, cr, ci);
+          xr[i + 1] = cr;
+          xi[i + 1] = ci;
+        }
+      }
+      double t = fmax(fabs(xr[i]), fabs(xi[i]));
+      if ((eps * t) * t > 1)
+        for (int j = i; j <= n; ++j) {
+          xr[j] /= t;
+          xi[j] /= t;
+        }
+    }
+  }
+  // back-transform: v = Z x ; re = col n-1, im = col n (eigenvalue wr + i*|wi|)
+  double nrm = 0.0;
+  for (int i = 0; i < p; ++i) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k <= n; ++k) {
+      a += Z[IX(i, k, ldz)] * xr[k];
+      b += Z[IX(i, k, ldz)] * xi[k];
+    }
+    out_re[i] = a;
+    out_im[i] = b;
+    nrm += a * a + b * b;
+  }
+  // dgeev: unit 2-norm, then rotate so the largest component is real
+  nrm = sqrt(nrm);
+  double inv = nrm > 0 ? 1.0 / nrm : 1.0;
+  int kmax = 0;
+  double best = -1.0;
+  for (int i = 0; i < p; ++i) {
+    out_re[i] *= inv;
+    out_im[i] *= inv;
+    double m2 = out_re[i] * out_re[i] + out_im[i] * out_im[i];
+    if (m2 > best) {
+      best = m2;
+      kmax = i;
+    }
+  }
+  double f = out_re[kmax], g = out_im[kmax], cs, sn;
+  if (g == 0.0) {
+    cs = 1.0;
+    sn = 0.0;
+  } else if (f == 0.0) {
+    cs = 0.0;
+    sn = copysign(1.0, g);
+  } else {
+    double d = sqrt(f * f + g * g);
+    cs = fabs(f) / d;
+    double rr = copysign(d, f);
+    sn = g / rr;
+  }
+  for (int i = 0; i < p; ++i) {
+    double a = out_re[i], b = out_im[i];
+    out_re[i] = cs * a + sn * b;
+    out_im[i] = cs * b - sn * a;
+  }
+  out_im[kmax] = 0.0;
+}
+
+}  // namespace gb

@@ -1,0 +1,379 @@
+// GEPP LU factorisation in u_f (reference densela.py:124-168).
+//
+//   MODE_H16: the reference's simulated half GEPP -- multiplier fl16(a/p),
+//             update fl16(a - fl16(l*u)), first-max pivot, whole-row swaps.
+//             Every element receives its updates in increasing k, so the
+//             blocked right-looking variant below (panel, row swaps, TRSM,
+//             trailing update applying k in order) is bit-identical to the
+//             unblocked reference loop.
+//   MODE_F32 / MODE_F64: LAPACK-style GEPP (?getrf): FMA updates, multipliers
+//             by the reciprocal pivot, zero pivots skipped and reported.
+//
+// Storage: row-major, leading dimension ld.  perm[i] = original row at pivot
+// position i (densela.py:137-140 converts LAPACK ipiv the same way).
+#pragma once
+#include "gb_ops.cuh"
+
+namespace gb {
+
+template <int M>
+struct LuT;
+template <>
+struct LuT<MODE_H16> {
+  using S = __half;  // global storage
+  using C = float;   // compute carrier (half-valued)
+  GB_DEVICE static S st(C x) { return __float2half_rn(x); }
+  GB_DEVICE static C ld(S x) { return __half2float(x); }
+  GB_DEVICE static S from_u(double x) { return __double2half(x); }
+  GB_DEVICE static C mult(C a, C p) { return h_div(a, p); }
+  GB_DEVICE static C upd(C a, C l, C u) { return h_sub(a, h_mul(l, u)); }
+  static constexpr bool kLapack = false;
+};
+template <>
+struct LuT<MODE_F32> {
+  using S = float;
+  using C = float;
+  GB_DEVICE static S st(C x) { return x; }
+  GB_DEVICE static C ld(S x) { return x; }
+  GB_DEVICE static S from_u(double x) { return __double2float_rn(x); }
+  GB_DEVICE static C mult(C a, C p) { return __fmul_rn(a, __frcp_rn(p)); }
+  GB_DEVICE static C upd(C a, C l, C u) { return __fmaf_rn(-l, u, a); }
+  static constexpr bool kLapack = true;
+};
+template <>
+struct LuT<MODE_F64> {
+  using S = double;
+  using C = double;
+  GB_DEVICE static S st(C x) { return x; }
+  GB_DEVICE static C ld(S x) { return x; }
+  GB_DEVICE static S from_u(double x) { return x; }
+  GB_DEVICE static C mult(C a, C p) { return __dmul_rn(a, __drcp_rn(p)); }
+  GB_DEVICE static C upd(C a, C l, C u) { return __fma_rn(-l, u, a); }
+  static constexpr bool kLapack = true;
+};
+
+// (|value|, index) pivot key: NaN beats everything (numpy argmax returns the
+// first NaN), then larger |value|, then the lower index.
+struct PivKey {
+  double v;
+  int i;
+  int nan;
+};
+GB_DEVICE bool piv_better(const PivKey& a, const PivKey& b) {
+  if (a.i < 0) return false;
+  if (b.i < 0) return true;
+  if (a.nan != b.nan) return a.nan > b.nan;
+  if (a.v != b.v) return a.v > b.v;
+  return a.i < b.i;
+}
+GB_DEVICE PivKey piv_shfl(const PivKey& k, int o) {
+  return PivKey{__shfl_xor_sync(0xffffffffu, k.v, o), __shfl_xor_sync(0xffffffffu, k.i, o),
+                __shfl_xor_sync(0xffffffffu, k.nan, o)};
+}
+// block-wide pivot search; every thread gets the result. scratch: 32 PivKey.
+__device__ inline PivKey block_pivot(PivKey k, PivKey* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    PivKey q = piv_shfl(k, o);
+    if (piv_better(q, k)) k = q;
+  }
+  __syncthreads();
+  if (lane == 0) scratch[wid] = k;
+  __syncthreads();
+  k = lane < nw ? scratch[lane] : PivKey{0.0, -1, 0};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    PivKey q = piv_shfl(k, o);
+    if (piv_better(q, k)) k = q;
+  }
+  __syncthreads();
+  return k;
+}
+GB_DEVICE PivKey make_key(double x, int i) {
+  PivKey k;
+  k.nan = (x != x);
+  k.v = k.nan ? 0.0 : fabs(x);
+  k.i = i;
+  return k;
+}
+
+// ---------------------------------------------------------------------------
+// one-CTA in-place GEPP on a buffer of carrier type C (smem or global).
+// Returns the first zero-pivot column, or -1.
+// ---------------------------------------------------------------------------
+template <int M>
+__device__ int lu_cta(typename LuT<M>::C* a, int n, int lda, int* perm, PivKey* scratch) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  __shared__ int s_p;
+  int zero = -1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    PivKey key{0.0, -1, 0};
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      PivKey c = make_key((double)a[(size_t)i * lda + k], i);
+      if (piv_better(c, key)) key = c;
+    }
+    key = block_pivot(key, scratch);
+    const int p = key.i;
+    const C piv = a[(size_t)p * lda + k];
+    const bool isz = (piv == C(0));
+    if (isz && zero < 0) zero = k;
+    if (isz && L::kLapack) continue;  // LAPACK: column already zero below
+    if (p != k) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        C t = a[(size_t)k * lda + j];
+        a[(size_t)k * lda + j] = a[(size_t)p * lda + j];
+        a[(size_t)p * lda + j] = t;
+      }
+      if (threadIdx.x == 0) {
+        int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x)
+      a[(size_t)i * lda + k] = L::mult(a[(size_t)i * lda + k], piv);
+    __syncthreads();
+    const int m = n - k - 1;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      int i = k + 1 + e / m, j = k + 1 + e % m;
+      a[(size_t)i * lda + j] = L::upd(a[(size_t)i * lda + j], a[(size_t)i * lda + k], a[(size_t)k * lda + j]);
+    }
+    __syncthreads();
+  }
+  (void)s_p;
+  return zero;
+}
+
+// ---------------------------------------------------------------------------
+// blocked GEPP kernels (large n)
+// ---------------------------------------------------------------------------
+struct LuStatus {
+  int zero_col;  // first zero pivot (or INT_MAX)
+  int pad;
+  unsigned long long amax_bits;  // max|A_uf| as ordered bits
+  unsigned long long umax_bits;  // max|U|
+};
+
+GB_DEVICE void atomic_max_abs(unsigned long long* p, double v) {
+  v = fabs(v);
+  if (v != v) v = __longlong_as_double(0x7ff0000000000000ull);  // NaN -> inf
+  atomicMax(p, (unsigned long long)__double_as_longlong(v));
+}
+
+// W = fl_uf(A) and the amax of the rounded matrix
+template <int M, class TA>
+__global__ void k_lu_convert(const TA* __restrict__ A, size_t lda, typename LuT<M>::S* W, size_t ldw,
+                             int n, LuStatus* st) {
+  using L = LuT<M>;
+  double m = 0.0;
+  size_t total = (size_t)n * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    size_t i = e / n, j = e % n;
+    typename L::S s = L::from_u((double)A[i * lda + j]);
+    W[i * ldw + j] = s;
+    double v = fabs((double)L::ld(s));
+    m = (v > m || v != v) ? v : m;
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_abs(&st->amax_bits, m);
+}
+
+// single-CTA panel factorisation on global memory: columns [k0, k0+nb)
+template <int M>
+__global__ void __launch_bounds__(1024) k_lu_panel(typename LuT<M>::S* W, size_t ld, int n, int k0, int nb,
+                                                   int* perm, int* piv, LuStatus* st) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  __shared__ PivKey scratch[32];
+  const int kend = min(n, k0 + nb);
+  for (int k = k0; k < kend; ++k) {
+    PivKey key{0.0, -1, 0};
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      PivKey c = make_key((double)L::ld(W[(size_t)i * ld + k]), i);
+      if (piv_better(c, key)) key = c;
+    }
+    key = block_pivot(key, scratch);
+    const int p = key.i;
+    const C pv = L::ld(W[(size_t)p * ld + k]);
+    const bool isz = (pv == C(0));
+    if (threadIdx.x == 0) {
+      if (isz) atomicMin(&st->zero_col, k);
+      piv[k - k0] = p;
+      if (p != k && !(isz && L::kLapack)) {
+        int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      } else {
+        piv[k - k0] = k;
+      }
+    }
+    if (isz && L::kLapack) {
+      __syncthreads();
+      continue;
+    }
+    if (p != k) {
+      for (int j = k0 + threadIdx.x; j < kend; j += blockDim.x) {
+        typename L::S t = W[(size_t)k * ld + j];
+        W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
+        W[(size_t)p * ld + j] = t;
+      }
+    }
+    __syncthreads();
+    const int w = kend - k - 1;  // remaining panel columns
+    // rows below k: multiplier then the panel-row update, one thread per row
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      typename L::S* row = W + (size_t)i * ld;
+      C l = L::mult(L::ld(row[k]), pv);
+      row[k] = L::st(l);
+      for (int j = 1; j <= w; ++j) {
+        C u = L::ld(W[(size_t)k * ld + k + j]);
+        row[k + j] = L::st(L::upd(L::ld(row[k + j]), l, u));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// apply the panel's row interchanges to the columns outside the panel
+template <int M>
+__global__ void k_lu_laswp(typename LuT<M>::S* W, size_t ld, int n, int k0, int nb, const int* piv) {
+  const int kend = min(n, k0 + nb);
+  const int outside = n - (kend - k0);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < outside; c += gridDim.x * blockDim.x) {
+    int j = c < k0 ? c : c + (kend - k0);
+    for (int k = k0; k < kend; ++k) {
+      int p = piv[k - k0];
+      if (p != k) {
+        auto t = W[(size_t)k * ld + j];
+        W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
+        W[(size_t)p * ld + j] = t;
+      }
+    }
+  }
+}
+
+// U12 = L11^-1 A12 with the exact per-element order (rows in increasing k)
+template <int M, int NB>
+__global__ void k_lu_trsm(typename LuT<M>::S* W, size_t ld, int n, int k0) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  __shared__ C l11[NB][NB + 1];
+  const int kend = min(n, k0 + NB);
+  const int nbr = kend - k0;
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    int r = e / NB, c = e % NB;
+    l11[r][c] = (r < nbr && c < nbr) ? L::ld(W[(size_t)(k0 + r) * ld + k0 + c]) : C(0);
+  }
+  __syncthreads();
+  for (int j = kend + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    C col[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) col[r] = r < nbr ? L::ld(W[(size_t)(k0 + r) * ld + j]) : C(0);
+#pragma unroll
+    for (int r = 1; r < NB; ++r) {
+#pragma unroll
+      for (int i = 0; i < r; ++i) col[r] = L::upd(col[r], l11[r][i], col[i]);
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r)
+      if (r < nbr) W[(size_t)(k0 + r) * ld + j] = L::st(col[r]);
+  }
+}
+
+// trailing update A22 -= L21 U12, k applied in order per element.
+// Tile 64 x 64, 256 threads, 4x4 elements per thread.
+template <int M, int NB>
+__global__ void __launch_bounds__(256) k_lu_gemm(typename LuT<M>::S* W, size_t ld, int n, int k0) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  constexpr int TM = 64, TN = 64;
+  __shared__ C ls[TM][NB + 1];
+  __shared__ C us[NB][TN + 1];
+  const int k1 = k0 + NB;
+  if (k1 >= n) return;
+  const int i0 = k1 + blockIdx.y * TM, j0 = k1 + blockIdx.x * TN;
+  if (i0 >= n || j0 >= n) return;
+  for (int e = threadIdx.x; e < TM * NB; e += blockDim.x) {
+    int r = e / NB, c = e % NB;
+    ls[r][c] = (i0 + r < n) ? L::ld(W[(size_t)(i0 + r) * ld + k0 + c]) : C(0);
+  }
+  for (int e = threadIdx.x; e < NB * TN; e += blockDim.x) {
+    int r = e / TN, c = e % TN;
+    us[r][c] = (j0 + c < n) ? L::ld(W[(size_t)(k0 + r) * ld + j0 + c]) : C(0);
+  }
+  __syncthreads();
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+  C acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
+      acc[a][b] = (i < n && j < n) ? L::ld(W[(size_t)i * ld + j]) : C(0);
+    }
+  if constexpr (L::kLapack) {
+    C s[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) s[a][b] = C(0);
+#pragma unroll 8
+    for (int k = 0; k < NB; ++k) {
+      C lv[4], uv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) lv[a] = ls[tr + 16 * a][k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) uv[b] = us[k][tc + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] = L::upd(s[a][b], -lv[a], uv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = acc[a][b] - s[a][b];
+  } else {
+#pragma unroll 4
+    for (int k = 0; k < NB; ++k) {
+      C lv[4], uv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) lv[a] = ls[tr + 16 * a][k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) uv[b] = us[k][tc + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = L::upd(acc[a][b], lv[a], uv[b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
+      if (i < n && j < n) W[(size_t)i * ld + j] = L::st(acc[a][b]);
+    }
+}
+
+// max |U| over the upper triangle
+template <int M>
+__global__ void k_lu_umax(const typename LuT<M>::S* W, size_t ld, int n, LuStatus* st) {
+  using L = LuT<M>;
+  double m = 0.0;
+  for (int i = blockIdx.x; i < n; i += gridDim.x)
+    for (int j = i + threadIdx.x; j < n; j += blockDim.x) {
+      double v = fabs((double)L::ld(W[(size_t)i * ld + j]));
+      m = (v > m || v != v) ? v : m;
+    }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_abs(&st->umax_bits, m);
+}
+
+}  // namespace gb

@@ -1,0 +1,138 @@
+// Execution teams.
+//
+// Every solver routine is written once against a Team:
+//   * CtaTeam  -- one CTA owns a whole system (batched mode, config 3 and the
+//                 small single systems); sync() is __syncthreads().
+//   * GridTeam -- every CTA of a cooperative (co-resident) grid works on one
+//                 large system; rows of length-n vectors are sliced across
+//                 CTAs, sync() is a grid barrier, and cross-CTA sums are
+//                 deterministic (per-CTA partials summed in rank order, so all
+//                 CTAs hold bit-identical scalars and take identical branches).
+#pragma once
+#include "gb_common.cuh"
+
+namespace gb {
+
+struct GridCtl {
+  unsigned int count;
+  unsigned int gen;
+  unsigned int pad[30];
+};
+
+GB_DEVICE unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+GB_DEVICE void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct CtaTeam {
+  static constexpr bool kGrid = false;
+  GB_DEVICE int size() const { return 1; }
+  GB_DEVICE int rank() const { return 0; }
+  GB_DEVICE bool leader() const { return true; }
+  GB_DEVICE void sync() { __syncthreads(); }
+  // rows [lo, hi) of a length-n vector owned by this CTA
+  GB_DEVICE void rows(int n, int& lo, int& hi) const {
+    lo = 0;
+    hi = n;
+  }
+  // after a block-level reduction of K values (all threads hold them), make
+  // them team-wide.  Nothing to do for a single CTA.
+  template <class T, int K>
+  GB_DEVICE void finish_sum(T (&v)[K]) {}
+  GB_DEVICE double finish_max(double v) { return v; }
+  // vector variant: local[K] in smem (this CTA's partials) -> out[K] in smem
+  template <class T>
+  __device__ void sum_vec(const T* local, T* out, int K) {
+    for (int i = threadIdx.x; i < K; i += blockDim.x) out[i] = local[i];
+    __syncthreads();
+  }
+};
+
+struct GridTeam {
+  static constexpr bool kGrid = true;
+  int G, r;
+  GridCtl* ctl;
+  double* partials;  // 2 buffers of G * kMaxK doubles
+  int kmax;
+  unsigned phase;
+
+  GB_DEVICE int size() const { return G; }
+  GB_DEVICE int rank() const { return r; }
+  GB_DEVICE bool leader() const { return r == 0; }
+
+  __device__ void sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned g = ld_acquire(&ctl->gen);
+      __threadfence();
+      unsigned arrived = atomicAdd(&ctl->count, 1u);
+      if (arrived == (unsigned)G - 1) {
+        atomicExch(&ctl->count, 0u);
+        __threadfence();
+        st_release(&ctl->gen, g + 1);
+      } else {
+        while (ld_acquire(&ctl->gen) == g) __nanosleep(20);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  GB_DEVICE void rows(int n, int& lo, int& hi) const {
+    int per = (n + G - 1) / G;
+    per = (per + 31) & ~31;
+    lo = min(n, r * per);
+    hi = min(n, lo + per);
+  }
+  GB_DEVICE double* buf() { return partials + (size_t)(phase & 1) * G * kmax; }
+
+  // v[] holds this CTA's block-reduced values in every thread.
+  template <class T, int K>
+  __device__ void finish_sum(T (&v)[K]) {
+    double* p = buf();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) p[(size_t)r * K + i] = (double)v[i];
+    }
+    sync();
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      T acc = T(0);
+      for (int g = lane; g < G; g += 32) acc += (T)__ldcg(p + (size_t)g * K + i);
+      v[i] = warp_sum(acc);
+    }
+    ++phase;
+  }
+  __device__ double finish_max(double v) {
+    double* p = buf();
+    if (threadIdx.x == 0) p[r] = v;
+    sync();
+    const int lane = threadIdx.x & 31;
+    double acc = -1.0;
+    for (int g = lane; g < G; g += 32) acc = nan_max(acc, __ldcg(p + g));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = nan_max(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    ++phase;
+    return acc;
+  }
+  // local[K] (smem, this CTA's partials) -> out[K] (smem) summed in rank order.
+  template <class T>
+  __device__ void sum_vec(const T* local, T* out, int K) {
+    double* p = buf();
+    for (int i = threadIdx.x; i < K; i += blockDim.x) p[(size_t)r * K + i] = (double)local[i];
+    sync();
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+      T acc = T(0);
+      for (int g = 0; g < G; ++g) acc += (T)__ldcg(p + (size_t)g * K + i);
+      out[i] = acc;
+    }
+    __syncthreads();
+    ++phase;
+  }
+};
+
+}  // namespace gb

@@ -1,0 +1,312 @@
+"""Mixed-precision iterative refinement drivers -- the drop-in API.
+
+Mirrors ``irkit.refine`` (reference refine.py:56-464): the same ``Method``,
+``RefineConfig`` fields and defaults, ``RefinementReport`` fields and the same
+decision rules.  The refinement loop stays on the host (north_star); each
+iteration is ONE device launch (``gb_refine_step``: residual-scaled
+correction solve by GCRO-DR / GMRES / LU substitution, the update, the forward
+error and the new residual with nbe/cbe), and only its scalars come back.
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .precision import Format, PrecisionTriple, squared_format
+
+__all__ = [
+    "Method",
+    "DivergenceReason",
+    "RefineConfig",
+    "RefinementReport",
+    "ConvergenceDecision",
+    "classify",
+    "sir",
+    "gmres_ir",
+    "rgmres_ir",
+    "solve",
+]
+
+
+class Method(enum.Enum):
+    SIR = "sir"
+    GMRES_IR = "gmres-ir"
+    SGMRES_IR = "sgmres-ir"
+    RGMRES_IR = "rgmres-ir"
+    RSGMRES_IR = "rsgmres-ir"
+
+    @classmethod
+    def parse(cls, name: str) -> "Method":
+        try:
+            return cls(name.strip().lower())
+        except ValueError:
+            raise ValueError(f"unknown method {name!r}; expected one of {[m.value for m in cls]}") from None
+
+    @property
+    def uses_gmres(self) -> bool:
+        return self in (Method.GMRES_IR, Method.SGMRES_IR)
+
+    @property
+    def uses_recycling(self) -> bool:
+        return self in (Method.RGMRES_IR, Method.RSGMRES_IR)
+
+    @property
+    def uniform_precision(self) -> bool:
+        return self in (Method.SGMRES_IR, Method.RSGMRES_IR)
+
+    @property
+    def code(self) -> int:
+        return {"sir": _lib.SIR, "gmres-ir": _lib.GMRES_IR, "sgmres-ir": _lib.SGMRES_IR,
+                "rgmres-ir": _lib.RGMRES_IR, "rsgmres-ir": _lib.RSGMRES_IR}[self.value]
+
+
+class DivergenceReason(enum.Enum):
+    I_MAX_EXCEEDED = "IMaxExceeded"
+    INNER_STAGNATION = "InnerStagnation"
+    ERROR_GROWTH = "ErrorGrowth"
+
+
+_DEFAULT_TAU = {Format.HALF: 1e-2, Format.SINGLE: 1e-4, Format.DOUBLE: 1e-8, Format.QUAD: 1e-8}
+
+
+@dataclass
+class RefineConfig:
+    """refine.py:100-134 (same fields, same defaults)."""
+
+    precisions: PrecisionTriple
+    method: Method = Method.GMRES_IR
+    m: int = 0
+    k: int = 0
+    tau: float | None = None
+    i_max: int = 10000
+    extra_precision_matvec: bool | None = None
+    c_conv: float = 2.0
+    max_cycles: int | None = None
+    reorthogonalize: bool = True
+    scale_diag: bool = False
+    collect_diagnostics: bool = False
+    restart_residual: str = "recurrence"
+    cycle_residual: str = "recurrence"
+
+    def resolved_tau(self) -> float:
+        return self.tau if self.tau is not None else _DEFAULT_TAU[self.precisions.u]
+
+    def resolved_extra_precision(self) -> bool:
+        if self.extra_precision_matvec is not None:
+            return self.extra_precision_matvec
+        return not self.method.uniform_precision
+
+    def matvec_format(self) -> Format:
+        u = self.precisions.u
+        return squared_format(u) if self.resolved_extra_precision() else u
+
+    def resolved_m(self, n: int) -> int:
+        return self.m if self.m else min(n, 40)
+
+    def resolved_max_cycles(self, n: int) -> int:
+        if self.max_cycles is not None:
+            return self.max_cycles
+        return max(1, math.ceil(10 * n / self.resolved_m(n)))
+
+
+@dataclass
+class RefinementReport:
+    """refine.py:137-160."""
+
+    converged: bool
+    steps: int
+    inner_iters: list[int]
+    nbe_history: list[float]
+    ferr_history: list[float]
+    divergence_reason: DivergenceReason | None = None
+    solution: np.ndarray | None = None
+    diagnostics: dict = field(default_factory=dict)
+
+    @property
+    def total_inner(self) -> int:
+        return sum(self.inner_iters)
+
+    @property
+    def nbe_final(self) -> float:
+        return self.nbe_history[-1] if self.nbe_history else float("nan")
+
+    @property
+    def ferr_final(self) -> float:
+        return self.ferr_history[-1] if self.ferr_history else float("nan")
+
+
+@dataclass
+class ConvergenceDecision:
+    state: str  # "continue" | "converged" | "diverged"
+    reason: DivergenceReason | None
+    nbe: float
+    cbe: float = float("nan")
+    ferr: float = float("nan")
+
+
+def classify(nbe: float, cbe: float, ferr: float, history: list[float], precisions: PrecisionTriple,
+             c_conv: float = 2.0, inner_stagnated: bool = False) -> ConvergenceDecision:
+    """The decision rules of check_convergence (refine.py:210-229) applied to
+    device-computed nbe / cbe (the residual itself never leaves the GPU)."""
+    gate = c_conv * precisions.u.unit_roundoff
+    worst = max(nbe, cbe, ferr if math.isfinite(ferr) else 0.0)
+    if math.isfinite(worst) and worst <= gate:
+        return ConvergenceDecision("converged", None, nbe, cbe, ferr)
+    if inner_stagnated:
+        return ConvergenceDecision("diverged", DivergenceReason.INNER_STAGNATION, nbe, cbe, ferr)
+    growth = 0
+    seq = history + [nbe]
+    for prev, cur in zip(seq[:-1], seq[1:]):
+        if not math.isfinite(cur) or (math.isfinite(prev) and cur >= 2.0 * prev):
+            growth += 1
+        else:
+            growth = 0
+    if growth >= 3:
+        return ConvergenceDecision("diverged", DivergenceReason.ERROR_GROWTH, nbe, cbe, ferr)
+    return ConvergenceDecision("continue", None, nbe, cbe, ferr)
+
+
+def make_options(cfg: RefineConfig, n: int, grid_ctas: int = 0) -> _lib.Options:
+    """Resolve a RefineConfig into the C-ABI option block (refine.py:327-353)."""
+    prec = cfg.precisions
+    m = cfg.resolved_m(n)
+    if not (1 <= m <= n):
+        raise ValueError(f"restart length m={m} must satisfy 1 <= m <= n={n}")
+    if cfg.method.uses_recycling and not (1 <= cfg.k < m):
+        raise ValueError("recycling methods need 1 <= k < m")
+    if not cfg.resolved_tau() > 0:
+        raise ValueError("tolerance tau must be positive")
+    if cfg.restart_residual != "recurrence" or cfg.cycle_residual != "recurrence":
+        raise NotImplementedError("explicit restart/cycle residuals are not built (SURVEY §8(f) item 2)")
+    o = _lib.Options()
+    o.uf, o.u, o.ur = prec.uf.code, prec.u.code, prec.ur.code
+    o.method = cfg.method.code
+    o.m, o.k = m, (cfg.k if cfg.method.uses_recycling else 0)
+    o.tau = cfg.resolved_tau()
+    o.max_cycles = cfg.resolved_max_cycles(n)
+    o.reorthogonalize = int(bool(cfg.reorthogonalize))
+    o.extra_precision = int(cfg.resolved_extra_precision())
+    o.grid_ctas = grid_ctas
+    o.lu_mode = 0
+    return o
+
+
+def _pow2_equilibrate(a: np.ndarray, b: np.ndarray):
+    """Two-sided power-of-two scaling (refine.py:261-270); exact in binary."""
+    row = np.max(np.abs(a), axis=1)
+    row[row == 0.0] = 1.0
+    dr = 2.0 ** (-np.round(np.log2(row)))
+    a1 = dr[:, None] * a
+    col = np.max(np.abs(a1), axis=0)
+    col[col == 0.0] = 1.0
+    dc = 2.0 ** (-np.round(np.log2(col)))
+    return a1 * dc[None, :], dr * b, dc
+
+
+def _round_u(x: np.ndarray, u: Format) -> np.ndarray:
+    if u is Format.SINGLE:
+        return x.astype(np.float32).astype(np.float64)
+    if u is Format.HALF:
+        return x.astype(np.float16).astype(np.float64)
+    return x
+
+
+def _refine(a, b, cfg: RefineConfig, *, trace: list | None = None, grid_ctas: int = 0) -> RefinementReport:
+    prec = cfg.precisions
+    if prec.u not in (Format.SINGLE, Format.DOUBLE):
+        raise NotImplementedError("working precision u must be single or double on this build")
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n = a.shape[0]
+    if a.ndim != 2 or a.shape != (n, n) or b.shape != (n,):
+        raise ValueError("need a square matrix and a matching right-hand side")
+    diagnostics: dict = {}
+    col_scale = None
+    if cfg.scale_diag:
+        # host-side input scaling by powers of two (exact); rounding to u of the
+        # scaled data is repeated on the device, as in refine.py:293-297
+        a, b, col_scale = _pow2_equilibrate(_round_u(a, prec.u), _round_u(b, prec.u))
+        diagnostics["equilibrated"] = True
+    opts = make_options(cfg, n, grid_ctas)
+    solver = _lib.Solver(n, opts)
+    try:
+        solver.set_system(a, b)
+        zero, growth = solver.factorize()
+        if zero >= 0:
+            return RefinementReport(False, 0, [], [], [], DivergenceReason.INNER_STAGNATION, None,
+                                    {"lu_failed": f"exact zero pivot at column {zero}", **diagnostics})
+        diagnostics["lu_growth"] = growth
+        if solver.initial_solution():
+            diagnostics["x0_reset"] = True
+        if not solver.reference_solution():
+            diagnostics["no_reference_solution"] = True
+        nbe_hist: list[float] = []
+        ferr_hist: list[float] = []
+        inner: list[int] = []
+        reason: DivergenceReason | None = DivergenceReason.I_MAX_EXCEEDED
+        converged = False
+        for _ in range(cfg.i_max):
+            info = solver.step()
+            if trace is not None:
+                cyc, keff = solver.last_cycles()
+                trace.append({"nu": info.nu, "cycles": cyc, "k_eff": keff, "applies": info.applies,
+                              "status": info.status, "ms": solver.last_step_ms})
+            if info.status & (_lib.ST_NU_ZERO | _lib.ST_NU_NONFINITE):
+                if info.status & _lib.ST_NU_ZERO:
+                    converged, reason = True, None
+                    inner.append(0)
+                    nbe_hist.append(0.0)
+                    ferr_hist.append(info.ferr)
+                else:
+                    reason = DivergenceReason.ERROR_GROWTH
+                break
+            inner.append(int(info.inner_iters))
+            stagnated = bool(info.status & _lib.ST_STAGNATED) and cfg.method is not Method.SIR
+            decision = classify(info.nbe, info.cbe, info.ferr, nbe_hist, prec, cfg.c_conv, stagnated)
+            nbe_hist.append(decision.nbe)
+            ferr_hist.append(info.ferr)
+            if decision.state == "converged":
+                converged, reason = True, None
+                break
+            if decision.state == "diverged":
+                reason = decision.reason
+                break
+        solution = solver.solution()
+        if col_scale is not None:
+            solution = col_scale * solution
+        return RefinementReport(converged, len(inner), inner, nbe_hist, ferr_hist,
+                                None if converged else reason, solution, diagnostics)
+    finally:
+        solver.close()
+
+
+def sir(a, b, cfg: RefineConfig) -> RefinementReport:
+    if cfg.method is not Method.SIR:
+        raise ValueError("sir() requires cfg.method == Method.SIR")
+    return _refine(a, b, cfg)
+
+
+def gmres_ir(a, b, cfg: RefineConfig) -> RefinementReport:
+    if not cfg.method.uses_gmres:
+        raise ValueError("gmres_ir() requires a GMRES-based method")
+    return _refine(a, b, cfg)
+
+
+def rgmres_ir(a, b, cfg: RefineConfig) -> RefinementReport:
+    if not cfg.method.uses_recycling:
+        raise ValueError("rgmres_ir() requires a recycling method")
+    return _refine(a, b, cfg)
+
+
+def solve(a, b, cfg: RefineConfig) -> RefinementReport:
+    """Dispatch on cfg.method (refine.py:458-464)."""
+    if cfg.method is Method.SIR:
+        return sir(a, b, cfg)
+    if cfg.method.uses_gmres:
+        return gmres_ir(a, b, cfg)
+    return rgmres_ir(a, b, cfg)
