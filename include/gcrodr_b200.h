@@ -86,6 +86,8 @@ gb_status gb_solver_destroy(gb_solver* s);
 
 /* refine.py:285-300 -- A, b rounded to u, ||A||_inf, ||b||_inf */
 gb_status gb_set_system(gb_solver* s, const double* a, const double* b);
+/* same with float64 inputs already resident in device memory */
+gb_status gb_set_system_device(gb_solver* s, const double* a_dev, const double* b_dev);
 
 /* densela.lu_factor (densela.py:124-168) on fl_u(A) rounded to u_f.
  * zero_col = first exact zero pivot (-1 if none), growth = max|U|/max|A| */
@@ -116,6 +118,9 @@ gb_status gb_apply_preconditioned(gb_solver* s, const double* v, double* w, int 
 gb_status gb_precond_rhs(gb_solver* s, const double* r, double* out, int fmt);
 gb_status gb_residual(gb_solver* s, const double* x, double* r, int fmt);
 gb_status gb_lu_solve(gb_solver* s, const double* b, double* x);
+
+/* number of kernels this library has launched (process-wide) */
+long long gb_launch_count(void);
 
 /* timing helper: device time (ms) of the last gb_refine_step / gb_factorize */
 double gb_last_step_ms(gb_solver* s);

@@ -8,6 +8,7 @@ There is no CPU fallback.
 """
 
 from .precision import Format, PrecisionTriple, squared_format
+from .batched import solve_batched
 from .refine import (
     ConvergenceDecision,
     DivergenceReason,

@@ -24,7 +24,7 @@ ST_NU_ZERO, ST_NU_NONFINITE = 256, 512
 
 EXPORTS = [
     "gb_version", "gb_last_error", "gb_device_count", "gb_solver_create", "gb_solver_destroy",
-    "gb_set_system", "gb_factorize", "gb_initial_solution", "gb_reference_solution",
+    "gb_set_system", "gb_set_system_device", "gb_launch_count", "gb_factorize", "gb_initial_solution", "gb_reference_solution",
     "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
     "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched",
@@ -84,6 +84,8 @@ def load(path: str | None = None):
         "gb_solver_create": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(Options), vp]),
         "gb_solver_destroy": (C.c_int, [vp]),
         "gb_set_system": (C.c_int, [vp, vp, vp]),
+        "gb_set_system_device": (C.c_int, [vp, vp, vp]),
+        "gb_launch_count": (C.c_longlong, []),
         "gb_factorize": (C.c_int, [vp, ip, dp]),
         "gb_initial_solution": (C.c_int, [vp, ip]),
         "gb_reference_solution": (C.c_int, [vp, ip]),
@@ -171,6 +173,10 @@ class Solver:
         b = np.ascontiguousarray(b, dtype=np.float64)
         self._keep = (a, b)
         _check(self.lib.gb_set_system(self.h, _ptr(a), _ptr(b)), "gb_set_system")
+
+    def set_system_device(self, a_ptr: int, b_ptr: int) -> None:
+        """float64 inputs already resident in device memory (e.g. torch tensors)."""
+        _check(self.lib.gb_set_system_device(self.h, C.c_void_p(a_ptr), C.c_void_p(b_ptr)), "gb_set_system_device")
 
     def factorize(self) -> tuple[int, float]:
         z, g = C.c_int(), C.c_double()

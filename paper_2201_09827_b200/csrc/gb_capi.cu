@@ -14,6 +14,11 @@ const VariantOps* gb_variant_d_f_f64() __attribute__((weak));
 const VariantOps* gb_variant_d_d_dd() __attribute__((weak));
 const VariantOps* gb_variant_d_d_f64() __attribute__((weak));
 
+long long* gb_launch_counter() {
+  static long long counter = 0;
+  return &counter;
+}
+
 namespace {
 const VariantOps* get_variant(const VariantOps* (*fn)(), std::string& why) {
   if (fn == nullptr) {
@@ -75,7 +80,7 @@ gb_status gb_solver_create(gb_solver** out, int n, const gb_options* opt, void* 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int want = o.grid_ctas > 0 ? o.grid_ctas : std::min(sms, std::max(2, (n + 127) / 128));
+    int want = o.grid_ctas > 0 ? o.grid_ctas : std::min(sms, std::max(2, (n + 63) / 64));
     s->G = std::min(want, sms);
   }
   if (cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess) {
@@ -101,15 +106,20 @@ gb_status gb_solver_destroy(gb_solver* s) {
   return GB_OK;
 }
 
-gb_status gb_set_system(gb_solver* s, const double* a, const double* b) {
+static gb_status set_system_any(gb_solver* s, const double* a, const double* b, int dev) {
   if (!s || !a || !b) return fail(GB_ERR_ARG, "null argument");
-  gb_status st = s->ops->set_system(s, a, b);
+  gb_status st = s->ops->set_system(s, a, b, dev);
   if (st == GB_OK) {
     s->have_system = true;
     s->have_lu = s->have_x0 = false;
   }
   return st;
 }
+gb_status gb_set_system(gb_solver* s, const double* a, const double* b) { return set_system_any(s, a, b, 0); }
+gb_status gb_set_system_device(gb_solver* s, const double* a_dev, const double* b_dev) {
+  return set_system_any(s, a_dev, b_dev, 1);
+}
+long long gb_launch_count(void) { return *gb_launch_counter(); }
 
 gb_status gb_factorize(gb_solver* s, int* zero_col, double* growth) {
   if (!s || !s->have_system) return fail(GB_ERR_STATE, "gb_set_system first");
@@ -186,18 +196,16 @@ double gb_last_factor_ms(gb_solver* s) { return s ? s->last_factor_ms : 0.0; }
 
 gb_status gb_solve_batched(int count, int n, const gb_options* opt, int i_max, double c_conv, const double* a,
                            const double* b, int on_device, gb_batch_out* out, double* device_ms, void* stream) {
-  (void)count;
-  (void)n;
-  (void)opt;
-  (void)i_max;
-  (void)c_conv;
-  (void)a;
-  (void)b;
-  (void)on_device;
-  (void)out;
-  (void)device_ms;
-  (void)stream;
-  return fail(GB_ERR_UNSUPPORTED, "batched mode not built yet");
+  if (!opt || !a || !b || !out || count < 1 || n < 2 || i_max < 1) return fail(GB_ERR_ARG, "bad arguments");
+  const gb_options& o = *opt;
+  if (!(o.m >= 1 && o.m <= n)) return fail(GB_ERR_ARG, "restart length m must satisfy 1 <= m <= n");
+  if (o.k > 32) return fail(GB_ERR_UNSUPPORTED, "recycle dimension k > 32 is not built");
+  if ((o.method == GB_RGMRES_IR || o.method == GB_RSGMRES_IR) && !(o.k >= 1 && o.k < o.m))
+    return fail(GB_ERR_ARG, "recycling methods need 1 <= k < m");
+  std::string why;
+  const VariantOps* ops = pick_variant(o, why);
+  if (!ops) return fail(GB_ERR_UNSUPPORTED, why);
+  return ops->batched(count, n, opt, i_max, c_conv, a, b, on_device, out, device_ms, (cudaStream_t)stream);
 }
 
 }  // extern "C"

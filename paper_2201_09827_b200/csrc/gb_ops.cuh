@@ -284,20 +284,79 @@ __host__ __device__ inline size_t trsv_smem_bytes(int nthreads) {
 // GEMV rows into the accumulator: y[i] = sum_j A[src(i), j] * v[j]
 // One warp per row; rows of a block distributed over the CTA's warps.
 // ---------------------------------------------------------------------------
-template <int M, class TA, class TV>
-__device__ typename Arith<M>::T row_dot(const TA* __restrict__ arow, const TV* __restrict__ v, int n) {
+// 16-byte vector of row elements
+template <class T>
+struct alignas(16) Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+
+// One warp computes sum_j a[j] * v[j] (mode M) and optionally sum |a||v|.
+// 128-bit loads, kU independent accumulators per lane (memory-level
+// parallelism), deterministic combine and warp tree.
+template <int M, bool kAbs, class TA, class TV>
+__device__ __forceinline__ typename Arith<M>::T row_dot_ex(const TA* __restrict__ arow, const TV* __restrict__ v,
+                                                           int n, double* absdot) {
   using Ar = Arith<M>;
-  typename Ar::T acc = Ar::zero();
+  using T = typename Ar::T;
+  constexpr int VW = Vec16<TA>::N;
+  constexpr int kU = 4;
   const int lane = threadIdx.x & 31;
-  for (int j = lane; j < n; j += 32) acc = Ar::mac(acc, (double)arow[j], to_d(v[j]));
-  // deterministic warp tree
+  T acc[kU];
+  double ab[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    acc[u] = Ar::zero();
+    ab[u] = 0.0;
+  }
+  const int nv = n / VW;
+  const Vec16<TA>* av = reinterpret_cast<const Vec16<TA>*>(arow);
+  int base = lane;
+  for (; base + 32 * (kU - 1) < nv; base += 32 * kU) {
+    Vec16<TA> a[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) a[u] = av[base + 32 * u];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const double x = (double)a[u].v[e];
+        const double y = to_d(v[(base + 32 * u) * VW + e]);
+        acc[u] = Ar::mac(acc[u], x, y);
+        if (kAbs) ab[u] = __fma_rn(fabs(x), fabs(y), ab[u]);
+      }
+    }
+  }
+  for (; base < nv; base += 32) {
+    Vec16<TA> a0 = av[base];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      const double x = (double)a0.v[e];
+      const double y = to_d(v[base * VW + e]);
+      acc[0] = Ar::mac(acc[0], x, y);
+      if (kAbs) ab[0] = __fma_rn(fabs(x), fabs(y), ab[0]);
+    }
+  }
+  for (int j = nv * VW + lane; j < n; j += 32) {
+    const double x = (double)arow[j];
+    const double y = to_d(v[j]);
+    acc[1] = Ar::mac(acc[1], x, y);
+    if (kAbs) ab[1] = __fma_rn(fabs(x), fabs(y), ab[1]);
+  }
+  T s = Ar::add(Ar::add(acc[0], acc[1]), Ar::add(acc[2], acc[3]));
   if constexpr (M == MODE_DD) {
-    acc = warp_sum_dd(acc);
+    s = warp_sum_dd(s);
   } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc = Ar::add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    for (int o = 16; o > 0; o >>= 1) s = Ar::add(s, __shfl_xor_sync(0xffffffffu, s, o));
   }
-  return acc;
+  if (kAbs) *absdot = warp_sum((ab[0] + ab[1]) + (ab[2] + ab[3]));
+  return s;
+}
+
+template <int M, class TA, class TV>
+__device__ __forceinline__ typename Arith<M>::T row_dot(const TA* __restrict__ arow, const TV* __restrict__ v, int n) {
+  return row_dot_ex<M, false>(arow, v, n, nullptr);
 }
 
 // ---------------------------------------------------------------------------

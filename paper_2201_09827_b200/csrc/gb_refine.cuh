@@ -35,35 +35,16 @@ __device__ ResidOut residual_check(Team& t, const TA* A, size_t lda, int n, cons
     double ca = 0.0;
     double ri;
     if (ur == UR_DD) {
-      dd acc{0.0, 0.0};
-      for (int j = lane; j < n; j += 32) {
-        double a = (double)ar[j], xv = (double)x[j];
-        acc = dd_add(acc, two_prod(a, xv));
-        ca = __fma_rn(fabs(a), fabs(xv), ca);
-      }
-      acc = warp_sum_dd(acc);
+      dd acc = row_dot_ex<MODE_DD, true>(ar, x, n, &ca);
       dd rr = dd_add(dd{(double)b[i], 0.0}, dd_neg(acc));
       ri = dd_val(rr);
     } else if (ur == UR_F64) {
-      double acc = 0.0;
-      for (int j = lane; j < n; j += 32) {
-        double a = (double)ar[j], xv = (double)x[j];
-        acc = __fma_rn(a, xv, acc);
-        ca = __fma_rn(fabs(a), fabs(xv), ca);
-      }
-      acc = warp_sum(acc);
+      double acc = row_dot_ex<MODE_F64, true>(ar, x, n, &ca);
       ri = __dsub_rn((double)b[i], acc);
     } else {
-      float acc = 0.f;
-      for (int j = lane; j < n; j += 32) {
-        float a = (float)ar[j], xv = (float)x[j];
-        acc = __fmaf_rn(a, xv, acc);
-        ca = __fma_rn(fabs((double)ar[j]), fabs((double)x[j]), ca);
-      }
-      acc = warp_sum(acc);
+      float acc = row_dot_ex<MODE_F32, true>(ar, x, n, &ca);
       ri = (double)__fsub_rn((float)b[i], acc);
     }
-    ca = warp_sum(ca);
     const double cd = ca + fabs((double)b[i]);
     if (lane == 0) r[i] = ri;
     rmax = nan_max(rmax, fabs(ri));

@@ -17,6 +17,9 @@
 using namespace gb;
 
 static thread_local std::string g_err;
+// kernels launched by this library (gb_launch_count); counted at launch sites
+extern long long* gb_launch_counter();
+static inline void count_launch(long long k = 1) { __atomic_fetch_add(gb_launch_counter(), k, __ATOMIC_RELAXED); }
 
 #define CK(x)                                                                  \
   do {                                                                         \
@@ -386,6 +389,249 @@ __global__ void __launch_bounds__(kThreads) k_lu_small(const TW* A, size_t lda, 
 }
 
 // ---------------------------------------------------------------------------
+// batched mode: one CTA per system, the whole refinement loop on the device
+// (refine.py:277-421 including the decision rules of check_convergence).
+// ---------------------------------------------------------------------------
+struct SlotLayout {
+  size_t stride;
+  size_t A, b, LU, lubuf, perm, xs, r, xref, rtmp, dtmp, V, w, xk, res, s, rhat, C, U, Cn, Un, Ut, Yt, Wd, Qd, H, R,
+      B, bc, dense, gram, ybuf, ctr, epoch, cyc_it, cyc_ke, keff_io, flags, has_xref, out, xa, xb, xyh, xyl, xperm;
+};
+
+struct BatchArgs {
+  int count, n, i_max;
+  double c_conv, u_unit;
+  const double* a;  // count x n x n
+  const double* b;  // count x n
+  char* slots;
+  SlotLayout L;
+  int* next;  // work counter
+  // outputs
+  int *converged, *steps, *reason, *inner, *flags;
+  double *nbe, *ferr, *x, *growth;
+  // options
+  int m, k, max_cycles, reorth, method, ur;
+  double tau;
+};
+
+template <class TW, class TF, int MV>
+__global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int UM = UfMode<TF>::M;
+  using L = LuT<UM>;
+  double* sm = reinterpret_cast<double*>(smem);
+  void* ops = smem + sm_doubles(B.m, B.k) * sizeof(double);
+  __shared__ int s_sys;
+  __shared__ PivKey pscr[32];
+  __shared__ double s_norm[2];
+  char* base = B.slots + (size_t)blockIdx.x * B.L.stride;
+  const SlotLayout& Ly = B.L;
+  const int n = B.n, ldv = (n + 31) & ~31;
+  Prob<TW, TF, MV> P;
+  memset(&P, 0, sizeof(P));
+  auto& K = P.K;
+  K.n = n;
+  K.ldv = ldv;
+  K.m = B.m;
+  K.k = B.k;
+  K.max_cycles = B.max_cycles;
+  K.tau = B.tau;
+  K.reorth = B.reorth;
+  K.recycling = B.method == METH_GCRODR;
+  TW* A = (TW*)(base + Ly.A);
+  K.sys = SysView<TW, TF>{n, (size_t)ldv, A, (size_t)ldv, (const TF*)(base + Ly.LU), (const int*)(base + Ly.perm)};
+  K.V = (TW*)(base + Ly.V);
+  K.w = (TW*)(base + Ly.w);
+  K.x = (TW*)(base + Ly.xk);
+  K.res = (TW*)(base + Ly.res);
+  K.s = (TW*)(base + Ly.s);
+  K.rhat = (TW*)(base + Ly.rhat);
+  K.C = (TW*)(base + Ly.C);
+  K.U = (TW*)(base + Ly.U);
+  K.Cn = (TW*)(base + Ly.Cn);
+  K.Un = (TW*)(base + Ly.Un);
+  K.Ut = (TW*)(base + Ly.Ut);
+  K.Yt = (TW*)(base + Ly.Yt);
+  K.Wd = (double*)(base + Ly.Wd);
+  K.Qd = (double*)(base + Ly.Qd);
+  K.H = (double*)(base + Ly.H);
+  K.R = (double*)(base + Ly.R);
+  K.B = (double*)(base + Ly.B);
+  K.bc = (double*)(base + Ly.bc);
+  K.dense = (double*)(base + Ly.dense);
+  K.gram = (double*)(base + Ly.gram);
+  K.gram_stride = (size_t)(B.m + B.k + 2) * (B.m + B.k + 2);
+  K.ybuf = (typename Arith<MV>::T*)(base + Ly.ybuf);
+  K.cycle_iters = (int*)(base + Ly.cyc_it);
+  K.cycle_keff = (int*)(base + Ly.cyc_ke);
+  K.keff_io = (int*)(base + Ly.keff_io);
+  P.b = (const TW*)(base + Ly.b);
+  P.xs = (TW*)(base + Ly.xs);
+  P.r = (double*)(base + Ly.r);
+  P.xref = (double*)(base + Ly.xref);
+  P.has_xref = (int*)(base + Ly.has_xref);
+  P.ur = B.ur;
+  P.method = B.method;
+  P.ctr = (unsigned long long*)(base + Ly.ctr);
+  P.epoch = (unsigned long long*)(base + Ly.epoch);
+  P.out = (gb_step_info*)(base + Ly.out);
+  P.flags = (int*)(base + Ly.flags);
+  CtaTeam t;
+  while (true) {
+    if (threadIdx.x == 0) s_sys = atomicAdd(B.next, 1);
+    __syncthreads();
+    const int sys = s_sys;
+    __syncthreads();
+    if (sys >= B.count) break;
+    const double* a = B.a + (size_t)sys * n * n;
+    const double* bb = B.b + (size_t)sys * n;
+    // A_u, b_u and the inf-norms (refine.py:285-300)
+    double rmax = 0.0, bmax = 0.0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = wid; i < n; i += nw) {
+      double rs = 0.0;
+      for (int j = lane; j < n; j += 32) {
+        TW v = (TW)a[(size_t)i * n + j];
+        A[(size_t)i * ldv + j] = v;
+        rs += fabs((double)v);
+      }
+      rs = warp_sum(rs);
+      rmax = (rs > rmax || rs != rs) ? rs : rmax;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      TW v = (TW)bb[i];
+      ((TW*)P.b)[i] = v;
+      double ab = fabs((double)v);
+      bmax = (ab > bmax || ab != ab) ? ab : bmax;
+    }
+    rmax = block_max(rmax, sm);
+    bmax = block_max(bmax, sm);
+    if (threadIdx.x == 0) {
+      s_norm[0] = rmax;
+      s_norm[1] = bmax;
+      K.keff_io[0] = 0;
+      K.keff_io[1] = 0;
+    }
+    __syncthreads();
+    P.normA = s_norm[0];
+    P.normB = s_norm[1];
+    // LU in u_f (densela.py:124-168) on the slot carrier buffer
+    typename L::C* lub = (typename L::C*)(base + Ly.lubuf);
+    double am = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      typename L::C v = L::ld(L::from_u((double)A[(size_t)(e / n) * ldv + e % n]));
+      lub[e] = v;
+      double x = fabs((double)v);
+      am = (x > am || x != x) ? x : am;
+    }
+    am = block_max(am, sm);
+    __syncthreads();
+    int* perm = (int*)(base + Ly.perm);
+    const int zero = lu_cta<UM>(lub, n, n, perm, pscr);
+    double um = 0.0;
+    TF* LUo = (TF*)(base + Ly.LU);
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      int i = e / n, j = e % n;
+      LUo[(size_t)i * ldv + j] = (TF)L::st(lub[e]);
+      if (j >= i) {
+        double x = fabs((double)lub[e]);
+        um = (x > um || x != x) ? x : um;
+      }
+    }
+    um = block_max(um, sm);
+    __syncthreads();
+    int flags = 0;
+    if (zero >= 0) {
+      if (threadIdx.x == 0) {
+        B.converged[sys] = 0;
+        B.steps[sys] = 0;
+        B.reason[sys] = 2;  // InnerStagnation
+        B.flags[sys] = 4;   // lu_failed
+        B.growth[sys] = NAN;
+      }
+      for (int i = threadIdx.x; i < n; i += blockDim.x) B.x[(size_t)sys * n + i] = NAN;
+      __syncthreads();
+      continue;
+    }
+    // x0 (refine.py:317-321)
+    x0_body(t, P, sm, ops);
+    __syncthreads();
+    if (P.flags[0]) flags |= 1;
+    // xref: double-double GEPP (n <= 600)
+    bool okx = dd_gepp_solve((const TW*)A, (size_t)ldv, P.b, n, (double*)(base + Ly.xa), (double*)(base + Ly.xb),
+                             (double*)(base + Ly.xyh), (double*)(base + Ly.xyl), (int*)(base + Ly.xperm), P.xref,
+                             pscr);
+    if (threadIdx.x == 0) P.has_xref[0] = okx ? 1 : 0;
+    __syncthreads();
+    if (!okx) flags |= 2;
+    // refinement loop with the reference's decision rules
+    int steps = 0, conv = 0, reason = 1, grow = 0;
+    double prev = 0.0;
+    for (int it = 0; it < B.i_max; ++it) {
+      step_body(t, P, sm, ops);
+      __syncthreads();
+      gb_step_info info = *P.out;
+      __syncthreads();
+      const size_t o = (size_t)sys * B.i_max + steps;
+      if (info.status & (RS_NU_ZERO | RS_NU_NONFINITE)) {
+        if (info.status & RS_NU_ZERO) {
+          if (threadIdx.x == 0) {
+            B.inner[o] = 0;
+            B.nbe[o] = 0.0;
+            B.ferr[o] = info.ferr;
+          }
+          steps++;
+          conv = 1;
+          reason = 0;
+        } else {
+          reason = 3;
+        }
+        break;
+      }
+      if (threadIdx.x == 0) {
+        B.inner[o] = info.inner_iters;
+        B.nbe[o] = info.nbe;
+        B.ferr[o] = info.ferr;
+      }
+      steps++;
+      // check_convergence (refine.py:210-229); Python max() semantics
+      double worst = info.nbe;
+      if (info.cbe > worst) worst = info.cbe;
+      const double f = isfinite(info.ferr) ? info.ferr : 0.0;
+      if (f > worst) worst = f;
+      const bool stag = (info.status & KS_STAGNATED) && B.method != METH_SIR;
+      if (isfinite(worst) && worst <= B.c_conv * B.u_unit) {
+        conv = 1;
+        reason = 0;
+        break;
+      }
+      if (stag) {
+        reason = 2;
+        break;
+      }
+      if (it > 0) {
+        if (!isfinite(info.nbe) || (isfinite(prev) && info.nbe >= 2.0 * prev)) grow++;
+        else grow = 0;
+      }
+      prev = info.nbe;
+      if (grow >= 3) {
+        reason = 3;
+        break;
+      }
+    }
+    if (threadIdx.x == 0) {
+      B.converged[sys] = conv;
+      B.steps[sys] = steps;
+      B.reason[sys] = conv ? 0 : reason;
+      B.flags[sys] = flags;
+      B.growth[sys] = am != 0.0 ? um / am : NAN;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) B.x[(size_t)sys * n + i] = (double)P.xs[i];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // arena
 // ---------------------------------------------------------------------------
 struct Arena {
@@ -446,7 +692,7 @@ struct gb_solver {
 
 struct VariantOps {
   gb_status (*setup)(gb_solver*);
-  gb_status (*set_system)(gb_solver*, const double*, const double*);
+  gb_status (*set_system)(gb_solver*, const double*, const double*, int);
   gb_status (*factor)(gb_solver*, int*, double*);
   gb_status (*x0)(gb_solver*, int*);
   gb_status (*xref)(gb_solver*, int*);
@@ -454,6 +700,8 @@ struct VariantOps {
   gb_status (*debug)(gb_solver*, const double*, double*, int what, int fmt);
   gb_status (*get_x)(gb_solver*, double*);
   gb_status (*get_lu)(gb_solver*, double*, long long*);
+  gb_status (*batched)(int, int, const gb_options*, int, double, const double*, const double*, int, gb_batch_out*,
+                       double*, cudaStream_t);
 };
 
 namespace {
@@ -545,6 +793,7 @@ struct Impl {
     size_t sm = smem_bytes(s);
     gb_status st = set_smem(kern, sm);
     if (st != GB_OK) return st;
+    count_launch();
     if (s->G == 1) {
       kern<<<1, kThreads, sm, s->stream>>>(args...);
       CK(cudaGetLastError());
@@ -632,14 +881,21 @@ struct Impl {
     return GB_OK;
   }
 
-  static gb_status set_system(gb_solver* s, const double* a, const double* b) {
+  static gb_status set_system(gb_solver* s, const double* a, const double* b, int on_device) {
     const int n = s->n;
-    double* bstage = s->rtmp;  // n doubles
-    CK(cudaMemcpyAsync(s->stage, a, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(bstage, b, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    const double* asrc = a;
+    const double* bsrc = b;
+    if (!on_device) {
+      double* bstage = s->rtmp;  // n doubles
+      CK(cudaMemcpyAsync(s->stage, a, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice, s->stream));
+      CK(cudaMemcpyAsync(bstage, b, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+      asrc = s->stage;
+      bsrc = bstage;
+    }
     CK(cudaMemsetAsync(s->norms, 0, 2 * sizeof(unsigned long long), s->stream));
     int blocks = std::min(1184, std::max(1, (n + 7) / 8));
-    k_set_system<TW><<<blocks, 256, 0, s->stream>>>(s->stage, n, (TW*)s->A, s->lda, bstage, (TW*)s->b, s->norms);
+    count_launch();
+    k_set_system<TW><<<blocks, 256, 0, s->stream>>>(asrc, n, (TW*)s->A, s->lda, bsrc, (TW*)s->b, s->norms);
     CK(cudaGetLastError());
     unsigned long long nb[2];
     CK(cudaMemcpyAsync(nb, s->norms, sizeof(nb), cudaMemcpyDeviceToHost, s->stream));
@@ -661,11 +917,13 @@ struct Impl {
       size_t sm = (size_t)n * n * sizeof(typename LuT<M>::C);
       gb_status e = set_smem(k_lu_small<M, TA>, sm);
       if (e != GB_OK) return e;
+      count_launch();
       k_lu_small<M, TA><<<1, kThreads, sm, s->stream>>>(A, lda, W, s->lda, n, perm, st);
       CK(cudaGetLastError());
       return GB_OK;
     }
     constexpr int NB = 32;
+    count_launch();
     k_lu_convert<M, TA><<<1184, 256, 0, s->stream>>>(A, lda, W, s->lda, n, st);
     CK(cudaGetLastError());
     // identity permutation
@@ -674,6 +932,7 @@ struct Impl {
     CK(cudaMemcpyAsync(perm, id.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     for (int k0 = 0; k0 < n; k0 += NB) {
+      count_launch(1 + (n - std::min(NB, n - k0) > 0) + 2 * (n - (k0 + NB) > 0));
       k_lu_panel<M><<<1, 1024, 0, s->stream>>>(W, s->lda, n, k0, NB, perm, piv, st);
       int outside = n - std::min(NB, n - k0);
       if (outside > 0) k_lu_laswp<M><<<(outside + 255) / 256, 256, 0, s->stream>>>(W, s->lda, n, k0, NB, piv);
@@ -685,6 +944,7 @@ struct Impl {
       }
     }
     CK(cudaGetLastError());
+    count_launch();
     k_lu_umax<M><<<std::min(n, 1184), 256, 0, s->stream>>>(W, s->lda, n, st);
     CK(cudaGetLastError());
     return GB_OK;
@@ -721,6 +981,7 @@ struct Impl {
   static gb_status xref(gb_solver* s, int* ok) {
     const int n = s->n;
     if (n <= 600) {
+      count_launch();
       k_xref_small<TW><<<1, kThreads, 0, s->stream>>>((const TW*)s->A, s->lda, (const TW*)s->b, n, s->xa, s->xb,
                                                      s->xyh, s->xyl, s->xperm, s->xref, s->has_xref);
       CK(cudaGetLastError());
@@ -792,6 +1053,7 @@ struct Impl {
   }
 
   static gb_status get_x(gb_solver* s, double* x) {
+    count_launch();
     k_to_f64<TW><<<64, 256, 0, s->stream>>>((const TW*)s->xs, s->n, s->dtmp);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(x, s->dtmp, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
@@ -813,8 +1075,156 @@ struct Impl {
     return GB_OK;
   }
 
+  static gb_status batched(int count, int n, const gb_options* o, int i_max, double c_conv, const double* a,
+                           const double* b, int on_device, gb_batch_out* out, double* device_ms, cudaStream_t st) {
+    if (n > 600) return fail(GB_ERR_UNSUPPORTED, "batched mode needs n <= 600 (dd GEPP reference solution)");
+    const int m = o->m, k = o->k, ldv = (n + 31) & ~31, S = m + k + 2;
+    SlotLayout Ly;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      off = (off + 255) & ~size_t(255);
+      size_t r = off;
+      off += bytes;
+      return r;
+    };
+    Ly.A = take(sizeof(TW) * (size_t)n * ldv);
+    Ly.b = take(sizeof(TW) * ldv);
+    Ly.LU = take(sizeof(TF) * (size_t)n * ldv);
+    Ly.lubuf = take(sizeof(double) * (size_t)n * n);
+    Ly.perm = take(sizeof(int) * ldv);
+    Ly.xs = take(sizeof(TW) * ldv);
+    Ly.r = take(sizeof(double) * ldv);
+    Ly.xref = take(sizeof(double) * ldv);
+    Ly.rtmp = take(sizeof(double) * ldv);
+    Ly.dtmp = take(sizeof(double) * ldv);
+    Ly.V = take(sizeof(TW) * (size_t)(m + 1) * ldv);
+    Ly.w = take(sizeof(TW) * ldv);
+    Ly.xk = take(sizeof(TW) * ldv);
+    Ly.res = take(sizeof(TW) * ldv);
+    Ly.s = take(sizeof(TW) * ldv);
+    Ly.rhat = take(sizeof(TW) * ldv);
+    Ly.C = take(sizeof(TW) * (size_t)(k + 1) * ldv);
+    Ly.U = take(sizeof(TW) * (size_t)(k + 1) * ldv);
+    Ly.Cn = take(sizeof(TW) * (size_t)(k + 1) * ldv);
+    Ly.Un = take(sizeof(TW) * (size_t)(k + 1) * ldv);
+    Ly.Ut = take(sizeof(TW) * (size_t)(k + 1) * ldv);
+    Ly.Yt = take(sizeof(TW) * (size_t)(k + 1) * ldv);
+    Ly.Wd = take(sizeof(double) * (size_t)(k + 1) * ldv);
+    Ly.Qd = take(sizeof(double) * (size_t)(k + 1) * ldv);
+    Ly.H = take(sizeof(double) * (size_t)(m + 1) * m);
+    Ly.R = take(sizeof(double) * (size_t)(m + 1) * m);
+    Ly.B = take(sizeof(double) * (size_t)(k + 1) * m);
+    Ly.bc = take(sizeof(double) * ((size_t)3 * S + 2 * (size_t)S * (k + 2) + 2 * (size_t)(k + 1) * (k + 1) + 64));
+    Ly.dense = take(sizeof(double) * ((size_t)10 * S * S + 24 * (size_t)S * (k + 3) + 4096));
+    Ly.gram = take(sizeof(double) * (size_t)2 * S * S);
+    Ly.ybuf = take(16 * (size_t)ldv);
+    Ly.ctr = take(32);
+    Ly.epoch = take(16);
+    Ly.cyc_it = take(sizeof(int) * (o->max_cycles + 4));
+    Ly.cyc_ke = take(sizeof(int) * (o->max_cycles + 4));
+    Ly.keff_io = take(16);
+    Ly.flags = take(16);
+    Ly.has_xref = take(16);
+    Ly.out = take(sizeof(gb_step_info));
+    Ly.xa = take(sizeof(double) * (size_t)n * n);
+    Ly.xb = take(sizeof(double) * (size_t)n * n);
+    Ly.xyh = take(sizeof(double) * ldv);
+    Ly.xyl = take(sizeof(double) * ldv);
+    Ly.xperm = take(sizeof(int) * ldv);
+    Ly.stride = (off + 255) & ~size_t(255);
+
+    const size_t sm = sm_doubles(m, k) * sizeof(double) + ops_bytes<TW, TF, MV>();
+    gb_status e = set_smem(k_batched<TW, TF, MV>, sm);
+    if (e != GB_OK) return e;
+    int dev = 0, sms = 148, per = 1;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_batched<TW, TF, MV>, kThreads, sm));
+    const int grid = std::max(1, std::min(count, sms * std::max(per, 1)));
+    // device buffers
+    char* slots = nullptr;
+    CK(cudaMalloc(&slots, Ly.stride * grid));
+    CK(cudaMemsetAsync(slots, 0, Ly.stride * grid, st));
+    const size_t na = (size_t)count * n * n, nb = (size_t)count * n;
+    const double *da = a, *db = b;
+    double *ta = nullptr, *tb = nullptr;
+    if (!on_device) {
+      CK(cudaMalloc(&ta, sizeof(double) * na));
+      CK(cudaMalloc(&tb, sizeof(double) * nb));
+      CK(cudaMemcpyAsync(ta, a, sizeof(double) * na, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(tb, b, sizeof(double) * nb, cudaMemcpyHostToDevice, st));
+      da = ta;
+      db = tb;
+    }
+    const size_t ints = (size_t)count * (5 + i_max) + 1, dbls = (size_t)count * (2 * i_max + n + 1);
+    int* ibuf = nullptr;
+    double* dbuf = nullptr;
+    CK(cudaMalloc(&ibuf, sizeof(int) * ints));
+    CK(cudaMalloc(&dbuf, sizeof(double) * dbls));
+    CK(cudaMemsetAsync(ibuf, 0, sizeof(int) * ints, st));
+    BatchArgs A;
+    A.count = count;
+    A.n = n;
+    A.i_max = i_max;
+    A.c_conv = c_conv;
+    A.u_unit = sizeof(TW) == 4 ? 5.9604644775390625e-08 : 1.1102230246251565e-16;
+    A.a = da;
+    A.b = db;
+    A.slots = slots;
+    A.L = Ly;
+    A.next = ibuf;
+    A.converged = ibuf + 1;
+    A.steps = A.converged + count;
+    A.reason = A.steps + count;
+    A.flags = A.reason + count;
+    A.inner = A.flags + count;
+    A.nbe = dbuf;
+    A.ferr = A.nbe + (size_t)count * i_max;
+    A.x = A.ferr + (size_t)count * i_max;
+    A.growth = A.x + (size_t)count * n;
+    A.m = m;
+    A.k = k;
+    A.max_cycles = o->max_cycles;
+    A.reorth = o->reorthogonalize;
+    A.method = o->method == GB_SIR ? METH_SIR
+               : (o->method == GB_GMRES_IR || o->method == GB_SGMRES_IR) ? METH_GMRES
+                                                                          : METH_GCRODR;
+    A.ur = o->ur == GB_QUAD ? UR_DD : (o->ur == GB_DOUBLE ? UR_F64 : UR_F32);
+    A.tau = o->tau;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    count_launch();
+    k_batched<TW, TF, MV><<<grid, kThreads, sm, st>>>(A);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, st));
+    // outputs
+    CK(cudaMemcpyAsync(out->converged, A.converged, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->steps, A.steps, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->reason, A.reason, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->flags, A.flags, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->inner, A.inner, sizeof(int) * count * i_max, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->nbe, A.nbe, sizeof(double) * count * i_max, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->ferr, A.ferr, sizeof(double) * count * i_max, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->x, A.x, sizeof(double) * count * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->growth, A.growth, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(slots);
+    cudaFree(ibuf);
+    cudaFree(dbuf);
+    if (ta) cudaFree(ta);
+    if (tb) cudaFree(tb);
+    return GB_OK;
+  }
+
   static const VariantOps* table() {
-    static const VariantOps t{setup, set_system, factor, x0, xref, step, debug, get_x, get_lu};
+    static const VariantOps t{setup, set_system, factor, x0, xref, step, debug, get_x, get_lu, batched};
     return &t;
   }
 };
