@@ -119,6 +119,11 @@ gb_status gb_precond_rhs(gb_solver* s, const double* r, double* out, int fmt);
 gb_status gb_residual(gb_solver* s, const double* x, double* r, int fmt);
 gb_status gb_lu_solve(gb_solver* s, const double* b, double* x);
 
+/* diagnostics: arm a phase-timer log of `cap` (tag, globaltimer ns) entries
+ * for subsequent launches; with out != NULL first copy the current log
+ * (1 + 2*cap words: count, then pairs) out.  cap = 0 disarms. */
+gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out);
+
 /* number of kernels this library has launched (process-wide) */
 long long gb_launch_count(void);
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "gb_set_system", "gb_set_system_device", "gb_launch_count", "gb_factorize", "gb_initial_solution", "gb_reference_solution",
     "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
-    "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched",
+    "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog",
 ]
 
 
@@ -99,6 +99,7 @@ def load(path: str | None = None):
         "gb_residual": (C.c_int, [vp, vp, vp, C.c_int]),
         "gb_lu_solve": (C.c_int, [vp, vp, vp]),
         "gb_last_step_ms": (C.c_double, [vp]),
+        "gb_debug_phaselog": (C.c_int, [vp, C.c_int, vp]),
         "gb_last_factor_ms": (C.c_double, [vp]),
         "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
                                        vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
@@ -239,6 +240,19 @@ class Solver:
 
     def lu_solve(self, b) -> np.ndarray:
         return self._vec_op(self.lib.gb_lu_solve, b)
+
+    def phaselog(self, cap: int = 0, read: bool = True):
+        """Diagnostics: read the current phase log (tag, ns) and re-arm with cap."""
+        out = None
+        if read and getattr(self, "_plog_cap", 0):
+            buf = np.zeros(1 + 2 * self._plog_cap, dtype=np.uint64)
+            _check(self.lib.gb_debug_phaselog(self.h, cap, _ptr(buf)), "gb_debug_phaselog")
+            k = int(buf[0])
+            out = [(int(buf[1 + 2 * i]), int(buf[2 + 2 * i])) for i in range(k)]
+        else:
+            _check(self.lib.gb_debug_phaselog(self.h, cap, None), "gb_debug_phaselog")
+        self._plog_cap = cap
+        return out
 
     @property
     def last_step_ms(self) -> float:

@@ -191,6 +191,23 @@ gb_status gb_lu_solve(gb_solver* s, const double* b, double* x) {
   return s->ops->debug(s, b, x, 3, s->o.uf);
 }
 
+gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out) {
+  if (!s) return fail(GB_ERR_ARG, "null solver");
+  if (out != nullptr && s->plog != nullptr) {
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(out, s->plog, sizeof(unsigned long long) * (1 + 2 * (size_t)s->plog_cap), cudaMemcpyDeviceToHost));
+  }
+  if (s->plog) cudaFree(s->plog);
+  s->plog = nullptr;
+  s->plog_cap = 0;
+  if (cap > 0) {
+    CK(cudaMalloc(&s->plog, sizeof(unsigned long long) * (1 + 2 * (size_t)cap)));
+    CK(cudaMemset(s->plog, 0, sizeof(unsigned long long) * (1 + 2 * (size_t)cap)));
+    s->plog_cap = cap;
+  }
+  return GB_OK;
+}
+
 double gb_last_step_ms(gb_solver* s) { return s ? s->last_step_ms : 0.0; }
 double gb_last_factor_ms(gb_solver* s) { return s ? s->last_factor_ms : 0.0; }
 

@@ -23,6 +23,28 @@
 
 namespace gb {
 
+// optional phase timers (globaltimer ns, CTA 0 thread 0); enabled per launch
+// by a non-null pointer.  slot 0 = count, then pairs (tag, t).
+struct PhaseLog {
+  unsigned long long* buf;
+  int cap;
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mark(const PhaseLog& L, int tag) {
+  if (L.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long i = L.buf[0];
+    if ((int)i < L.cap) {
+      L.buf[1 + 2 * i] = (unsigned long long)tag;
+      L.buf[2 + 2 * i] = gtimer();
+      L.buf[0] = i + 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // rounding
 // ---------------------------------------------------------------------------

@@ -156,6 +156,7 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
   t.rows(n, lo, hi);
   for (int j = 0; j < mb; ++j) {
     TW* vj = colp(K.V, ldv, j);
+    mark(ts.log, 20);
     apply_A(t, K, ts, vj, K.w, smem_ops, applies);
     // deflation against C: one CGS projection, sequential subtraction
     if (kc > 0) {
@@ -169,7 +170,9 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
         for (int i = threadIdx.x; i < kc; i += blockDim.x) K.B[IX(i, j, K.k + 1)] = tmp[i];
       __syncthreads();
     }
+    mark(ts.log, 21);
     const double wnorm0 = team_nrm2<TW>(t, K.w, n, red);
+    mark(ts.log, 22);
     // MGS: h_i = v_i . w ; w -= h_i v_i  (axpy fused with the next dot)
     double hprev = 0.0;
     for (int i = 0; i <= j; ++i) {
@@ -193,7 +196,9 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
       const TW* vp = colp(K.V, ldv, j);
       for (int r = lo + threadIdx.x; r < hi; r += blockDim.x) K.w[r] = F::axpy(-hprev, vp[r], K.w[r]);
     }
+    mark(ts.log, 23);
     double hlast = team_nrm2<TW>(t, K.w, n, red);
+    mark(ts.log, 24);
     if (K.reorth && hlast < sqrt_u * wnorm0) {
       for (int i = 0; i <= j; ++i) {
         const TW* vi = colp(K.V, ldv, i);
@@ -250,6 +255,7 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
     }
     const double estimate = fabs(g[j + 1]);
     co.steps = j + 1;
+    mark(ts.log, 25);
     __syncthreads();
     if (hlast == 0.0) {
       co.breakdown = co.converged = true;

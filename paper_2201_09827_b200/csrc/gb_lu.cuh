@@ -362,6 +362,17 @@ __global__ void __launch_bounds__(256) k_lu_gemm(typename LuT<M>::S* W, size_t l
     }
 }
 
+// dd-exact reciprocals of diag(U): 1/U_ii = rh + rl
+template <class S>
+__global__ void k_lu_rcp(const S* W, size_t ld, int n, double* rh, double* rl) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double d = to_d(W[(size_t)i * ld + i]);
+    dd q = dd_div(dd{1.0, 0.0}, dd{d, 0.0});
+    rh[i] = q.hi;
+    rl[i] = q.lo;
+  }
+}
+
 // max |U| over the upper triangle
 template <int M>
 __global__ void k_lu_umax(const typename LuT<M>::S* W, size_t ld, int n, LuStatus* st) {

@@ -52,6 +52,7 @@ struct Arith<MODE_F64> {
   GB_DEVICE static T add(T a, T b) { return __dadd_rn(a, b); }
   GB_DEVICE static T sub(T a, T b) { return __dsub_rn(a, b); }
   GB_DEVICE static T div(T y, double u) { return __ddiv_rn(y, u); }
+  GB_DEVICE static T mul_rcp(T y, double rh, double) { return __dmul_rn(y, rh); }
   GB_DEVICE static double val(T x) { return x; }
   GB_DEVICE static T shfl(T x, int src) { return __shfl_sync(0xffffffffu, x, src); }
   GB_DEVICE static T ld(const T* p) { return __ldcg(p); }
@@ -68,6 +69,7 @@ struct Arith<MODE_F32> {
   GB_DEVICE static T add(T a, T b) { return __fadd_rn(a, b); }
   GB_DEVICE static T sub(T a, T b) { return __fsub_rn(a, b); }
   GB_DEVICE static T div(T y, double u) { return __fdiv_rn(y, (float)u); }
+  GB_DEVICE static T mul_rcp(T y, double rh, double) { return __fmul_rn(y, (float)rh); }
   GB_DEVICE static double val(T x) { return (double)x; }
   GB_DEVICE static T shfl(T x, int src) { return __shfl_sync(0xffffffffu, x, src); }
   GB_DEVICE static T ld(const T* p) { return __ldcg(p); }
@@ -85,6 +87,7 @@ struct Arith<MODE_H16> {
   GB_DEVICE static T add(T a, T b) { return h_add(a, b); }
   GB_DEVICE static T sub(T a, T b) { return h_sub(a, b); }
   GB_DEVICE static T div(T y, double u) { return h_div(y, (float)u); }
+  GB_DEVICE static T mul_rcp(T y, double, double) { return y; }  // never used (exact order)
   GB_DEVICE static double val(T x) { return (double)x; }
   GB_DEVICE static T shfl(T x, int src) { return __shfl_sync(0xffffffffu, x, src); }
   GB_DEVICE static T ld(const T* p) { return __ldcg(p); }
@@ -101,6 +104,7 @@ struct Arith<MODE_DD> {
   GB_DEVICE static T add(T a, T b) { return dd_add(a, b); }
   GB_DEVICE static T sub(T a, T b) { return dd_sub(a, b); }
   GB_DEVICE static T div(T y, double u) { return dd_div(y, dd{u, 0.0}); }
+  GB_DEVICE static T mul_rcp(T y, double rh, double rl) { return dd_mul(y, dd{rh, rl}); }
   GB_DEVICE static double val(T x) { return dd_val(x); }
   GB_DEVICE static T shfl(T x, int src) {
     return dd{__shfl_sync(0xffffffffu, x.hi, src), __shfl_sync(0xffffffffu, x.lo, src)};
@@ -110,6 +114,11 @@ struct Arith<MODE_DD> {
     return dd{v.x, v.y};
   }
 };
+
+template <class T>
+GB_DEVICE T sel(bool c, T a, T b) { return c ? a : b; }
+template <>
+GB_DEVICE dd sel<dd>(bool c, dd a, dd b) { return dd{c ? a.hi : b.hi, c ? a.lo : b.lo}; }
 
 // tile element type: factors held at u_f width fit a float tile exactly
 template <class TF>
@@ -132,6 +141,10 @@ struct SysView {
   size_t ldf;
   const TF* LU;
   const int* perm;
+  // reciprocals of diag(U) (dd-exact hi/lo), used by the non-exact modes to
+  // keep divisions off the substitution's critical path; nullptr -> divide
+  const double* rcp_hi;
+  const double* rcp_lo;
 };
 
 // progress counters of the flag-based TRSV (one per direction)
@@ -139,11 +152,18 @@ struct TrsvSync {
   unsigned long long* fwd;
   unsigned long long* bwd;
   unsigned long long epoch;  // call index; identical in all CTAs
+  PhaseLog log;              // optional phase timers
+  unsigned long long* stamps = nullptr;  // diagnostics: per block (deps seen, published)
 };
 
 GB_DEVICE unsigned long long ld_acquire64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+GB_DEVICE unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 GB_DEVICE void st_release64(unsigned long long* p, unsigned long long v) {
@@ -156,128 +176,172 @@ GB_DEVICE void wait_progress(const unsigned long long* ctr, unsigned long long t
   if constexpr (Team::kGrid) {
     if (*cache >= target) return;
     unsigned long long v;
-    while ((v = ld_acquire64(ctr)) < target) __nanosleep(32);
+    while ((v = ld_relaxed64(ctr)) < target) __nanosleep(16);
+    fence_acq_rel();
     *cache = v;
   }
 }
 
 // ---------------------------------------------------------------------------
-// triangular solves over row blocks.
-//   y (in: right-hand side in accumulator type, out: solution), length n.
-//   Lower: unit diagonal, column order 0..i-1.  Upper: columns n-1..i+1 then
-//   divide by U_ii.  kSplit: number of warps that split the off-diagonal
-//   columns of a row block (1 keeps the exact per-element order).
+// triangular solves: warp-owned 32-row blocks, wavefront over the whole team.
+//   Row block b (32 rows) belongs to warp b mod W of the team (W = CTAs x
+//   warps), processed in the sweep order; each lane owns one row and walks the
+//   columns of its row in the reference's column-sweep order (lower: 0..i-1,
+//   upper: n-1..i+1 then the division), so the exact modes (H16) reproduce the
+//   reference bit for bit.  A block is published with one monotone progress
+//   counter per direction (st.release; consumers poll relaxed + one fence);
+//   the next tile's loads are issued before the wait (software pipelining).
+//   y: in = right-hand side (accumulator type), out = solution.
 // ---------------------------------------------------------------------------
+template <class TT, class TF>
+GB_DEVICE void tile_regs(TT (&v)[32], const TF* __restrict__ LU, size_t ldf, int n, int r0, int c0) {
+  const int gc = c0 + (threadIdx.x & 31);
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    const int gr = r0 + rr;
+    v[rr] = (gr < n && gc < n) ? (TT)to_d(LU[(size_t)gr * ldf + gc]) : TT(0);
+  }
+}
+template <class TT>
+GB_DEVICE void tile_store(TT* tile, const TT (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = v[rr];
+}
+
+// intra-CTA progress (CtaTeam): shared-memory counter
+struct CtaProgress {
+  volatile unsigned long long v;
+};
+
+
+template <class Team>
+GB_DEVICE void wait_ctr(unsigned long long* gctr, volatile unsigned long long* sctr, unsigned long long target,
+                        unsigned long long& cache) {
+  if (cache >= target) return;
+  unsigned long long v;
+  if constexpr (Team::kGrid) {
+    while ((v = ld_relaxed64(gctr)) < target) __nanosleep(8);
+    fence_acq_rel();
+  } else {
+    while ((v = *sctr) < target) {
+    }
+    __threadfence_block();
+  }
+  cache = v;
+}
+
 template <int M, class Team, class TF, bool kLower>
-__device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf,
-                            typename Arith<M>::T* y, const TrsvSync& ts, void* smem_raw) {
+__device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename Arith<M>::T* y,
+                            const TrsvSync& ts, void* smem_raw, const double* rcph = nullptr,
+                            const double* rcpl = nullptr) {
   using Ar = Arith<M>;
   using T = typename Ar::T;
-  const int nb = (n + kRB - 1) / kRB;
+  using TT = typename TileT<TF>::T;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const int split = Ar::kExactOrder ? 1 : nw;
-  // smem: per warp a 32x33 tile (fp64 factors keep a double tile) + partials
-  using TT = typename TileT<TF>::T;
-  TT* tiles = reinterpret_cast<TT*>(smem_raw);
-  T* parts = reinterpret_cast<T*>(tiles + nw * 32 * 33);
-  TT* tile = tiles + wid * 32 * 33;
-  unsigned long long* ctr = kLower ? ts.fwd : ts.bwd;
-  const unsigned long long base = ts.epoch * (unsigned long long)nb;
-  __shared__ unsigned long long cache;
-  if (threadIdx.x == 0) {
-    cache = 0;
+  const int nb = (n + 31) / 32;
+  TT* tile = reinterpret_cast<TT*>(smem_raw) + wid * 32 * 33;
+  unsigned long long* gctr = kLower ? ts.fwd : ts.bwd;
+  __shared__ CtaProgress sprog[2];
+  volatile unsigned long long* sctr = &sprog[kLower ? 0 : 1].v;
+  const unsigned long long base = Team::kGrid ? ts.epoch * (unsigned long long)nb : 0ull;
+  if constexpr (!Team::kGrid) {
+    if (threadIdx.x == 0) *sctr = 0ull;
+  }
+  __syncthreads();
+  unsigned long long cache = 0;
+  if (!kLower && Team::kGrid) {
     // the backward sweep starts from the bottom of the forward result
-    if (!kLower) {
-      unsigned long long c2 = 0;
-      wait_progress<Team>(ts.fwd, base + (unsigned long long)nb, &c2);
+    if (lane == 0) wait_ctr<Team>(ts.fwd, nullptr, base + (unsigned long long)nb, cache);
+    cache = 0;
+    __syncwarp();
+  }
+  const int W = t.size() * nw;
+  const int gw = t.rank() * nw + wid;
+  for (int s = gw; s < nb; s += W) {
+    const int b = kLower ? s : nb - 1 - s;
+    const int row0 = b * 32;
+    const int row = row0 + lane;
+    const bool rv = row < n;
+    T acc = rv ? Ar::ld(y + row) : Ar::zero();
+    const int noff = kLower ? b : nb - 1 - b;
+    TT v[32];
+    // first off-diagonal tile (or the diagonal tile) prefetched into registers;
+    // each iteration stores the current tile and prefetches the next one
+    tile_regs(v, LU, ldf, n, row0, noff > 0 ? (kLower ? 0 : nb - 1) * 32 : row0);
+    for (int q = 0; q < noff; ++q) {
+      const int cb = kLower ? q : nb - 1 - q;
+      const int c0 = cb * 32;
+      __syncwarp();
+      tile_store(tile, v);
+      tile_regs(v, LU, ldf, n, row0, q + 1 < noff ? (kLower ? q + 1 : nb - 2 - q) * 32 : row0);
+      // every lane polls: a single spinning lane costs ~9 us of warp
+      // reconvergence per wait on sm_100a (measured, tools/micro/trsv.cu)
+      wait_ctr<Team>(gctr, sctr, base + (unsigned long long)(q + 1), cache);
+      if (ts.stamps != nullptr && lane == 0 && q + 1 == noff) ts.stamps[3 * s + 2] = gtimer();
+      __syncwarp();
+      const T yv = (c0 + lane < n) ? Ar::ld(y + c0 + lane) : Ar::zero();
+      if (kLower) {
+        // branch-free: divergence inside these loops costs a warp
+        // reconvergence per step on sm_100a
+#pragma unroll 8
+        for (int jj = 0; jj < 32; ++jj) {
+          const T yj = Ar::shfl(yv, jj);
+          acc = sel(c0 + jj < n, Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj), acc);
+        }
+      } else {
+#pragma unroll 8
+        for (int jj = 31; jj >= 0; --jj) {
+          const T yj = Ar::shfl(yv, jj);
+          acc = sel(c0 + jj < n, Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj), acc);
+        }
+      }
+    }
+    if (ts.stamps != nullptr && lane == 0) ts.stamps[3 * s] = gtimer();
+    // diagonal block (its tile is already in v)
+    __syncwarp();
+    tile_store(tile, v);
+    __syncwarp();
+    if (kLower) {
+      for (int jj = 0; jj < 32; ++jj) {
+        const T yj = Ar::shfl(acc, jj);
+        acc = sel(lane > jj, Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj), acc);
+      }
+    } else {
+      const bool use_rcp = !Ar::kExactOrder && rcph != nullptr;
+      double rh = 0.0, rl = 0.0;
+      if (use_rcp && rv) {
+        rh = __ldg(rcph + row);
+        rl = rcpl != nullptr ? __ldg(rcpl + row) : 0.0;
+      }
+      const double dg = (double)tile[lane * 33 + lane];
+      for (int jj = 31; jj >= 0; --jj) {
+        const T dv = use_rcp ? Ar::mul_rcp(acc, rh, rl) : Ar::div(acc, dg);
+        acc = sel(lane == jj && rv, dv, acc);
+        const T yj = Ar::shfl(acc, jj);
+        acc = sel(lane < jj && row0 + jj < n, Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj), acc);
+      }
+    }
+    if (ts.stamps != nullptr && lane == 0) ts.stamps[3 * s + 1] = gtimer();
+    if (rv) y[row] = acc;
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (Team::kGrid) {
+        __threadfence();
+        st_release64(gctr, base + (unsigned long long)(s + 1));
+      } else {
+        __threadfence();  // y goes through L2: consumers read it with ld.cg
+        *sctr = (unsigned long long)(s + 1);
+      }
     }
   }
   __syncthreads();
-
-  const int G = t.size(), r = t.rank();
-  for (int s = r; s < nb; s += G) {
-    const int b = kLower ? s : nb - 1 - s;
-    const int row = b * kRB + lane;
-    const bool rv = row < n;
-    T acc = Ar::zero();
-    if (wid < split) {
-      if (wid == 0 && rv) acc = Ar::ld(y + row);
-      // off-diagonal column blocks handled by this warp, in order
-      const int ncb = kLower ? b : nb - 1 - b;  // number of off-diagonal blocks
-      for (int q = wid; q < ncb; q += split) {
-        const int cb = kLower ? q : nb - 1 - q;
-        // wait until column block cb is final
-        if (lane == 0) wait_progress<Team>(ctr, base + (unsigned long long)(q + 1), &cache);
-        __syncwarp();
-        // stage the 32x32 tile (rows of this block, columns of cb) coalesced
-        const int c0 = cb * kRB;
-        for (int rr = 0; rr < 32; ++rr) {
-          int gr = b * kRB + rr, gc = c0 + lane;
-          TT v = TT(0);
-          if (gr < n && gc < n) v = (TT)to_d(LU[(size_t)gr * ldf + gc]);
-          tile[rr * 33 + lane] = v;
-        }
-        T yv = (c0 + lane < n) ? Ar::ld(y + c0 + lane) : Ar::zero();
-        __syncwarp();
-        if (kLower) {
-          for (int jj = 0; jj < 32; ++jj) {
-            T yj = Ar::shfl(yv, jj);
-            if (rv && c0 + jj < n) acc = Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj);
-          }
-        } else {
-          for (int jj = 31; jj >= 0; --jj) {
-            T yj = Ar::shfl(yv, jj);
-            if (rv && c0 + jj < n) acc = Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj);
-          }
-        }
-        __syncwarp();
-      }
-      if (split > 1) parts[wid * 32 + lane] = acc;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      if (split > 1) {
-        acc = parts[lane];
-        for (int w = 1; w < split; ++w) acc = Ar::add(acc, parts[w * 32 + lane]);
-      }
-      // diagonal block
-      for (int rr = 0; rr < 32; ++rr) {
-        int gr = b * kRB + rr, gc = b * kRB + lane;
-        TT v = TT(0);
-        if (gr < n && gc < n) v = (TT)to_d(LU[(size_t)gr * ldf + gc]);
-        tile[rr * 33 + lane] = v;
-      }
-      __syncwarp();
-      if (kLower) {
-        for (int jj = 0; jj < 32; ++jj) {
-          T yj = Ar::shfl(acc, jj);
-          if (rv && lane > jj) acc = Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj);
-        }
-      } else {
-        for (int jj = 31; jj >= 0; --jj) {
-          if (lane == jj && rv) acc = Ar::div(acc, (double)tile[lane * 33 + lane]);
-          T yj = Ar::shfl(acc, jj);
-          if (rv && lane < jj && b * kRB + jj < n)
-            acc = Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj);
-        }
-      }
-      if (rv) y[row] = acc;
-      __syncwarp();
-      if constexpr (Team::kGrid) {
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release64(ctr, base + (unsigned long long)(s + 1));
-      }
-    }
-    __syncthreads();
-  }
 }
 
 template <int M, class TF>
 __host__ __device__ inline size_t trsv_smem_bytes(int nthreads) {
-  return (size_t)(nthreads / 32) * 32 * 33 * sizeof(typename TileT<TF>::T) +
-         (size_t)(nthreads / 32) * 32 * sizeof(typename Arith<M>::T);
+  return (size_t)(nthreads / 32) * 32 * 33 * sizeof(typename TileT<TF>::T);
 }
 
 // ---------------------------------------------------------------------------
@@ -369,38 +433,35 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
                          TW* w, typename Arith<M>::T* ybuf, TrsvSync& ts, void* smem) {
   using Ar = Arith<M>;
   const int n = s.n;
-  const int nb = (n + kRB - 1) / kRB;
-  const int G = t.size(), r = t.rank();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  // 1. right-hand side in permuted order, blocks owned as in the forward solve
-  for (int b = r; b < nb; b += G) {
-    for (int rr = wid; rr < kRB; rr += nw) {
-      int i = b * kRB + rr;
-      if (i >= n) break;
-      int src = s.perm[i];
-      typename Ar::T val;
-      if (v != nullptr) {
-        val = row_dot<M>(s.A + (size_t)src * s.lda, v, n);
-      } else {
-        val = Ar::from(to_d(rvec[src]));
-      }
-      if (lane == 0) ybuf[i] = val;
+  mark(ts.log, 10);
+  // 1. right-hand side in permuted order over the team's row slices
+  int lo, hi;
+  t.rows(n, lo, hi);
+  for (int i = lo + wid; i < hi; i += nw) {
+    const int src = s.perm[i];
+    typename Ar::T val;
+    if (v != nullptr) {
+      val = row_dot<M>(s.A + (size_t)src * s.lda, v, n);
+    } else {
+      val = Ar::from(to_d(rvec[src]));
     }
-  }
-  __syncthreads();
-  // 2. forward (unit lower) then backward (upper)
-  trsv_blocks<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem);
-  trsv_blocks<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem);
-  ts.epoch++;
-  // 3. round to u: each CTA writes the rows it finalised in the backward pass
-  for (int q = r; q < nb; q += G) {
-    int b = nb - 1 - q;
-    for (int rr = threadIdx.x; rr < kRB; rr += blockDim.x) {
-      int i = b * kRB + rr;
-      if (i < n) w[i] = (TW)Ar::val(Ar::ld(ybuf + i));
-    }
+    if (lane == 0) ybuf[i] = val;
   }
   t.sync();
+  mark(ts.log, 11);
+  // 2. forward (unit lower) then backward (upper)
+  trsv_blocks<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem);
+  mark(ts.log, 12);
+  trsv_blocks<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.rcp_hi, s.rcp_lo);
+  mark(ts.log, 13);
+  ts.epoch++;
+  // 3. round to u (rows of this CTA's slice; the backward sweep is complete
+  // once the whole team passed the barrier)
+  t.sync();
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) w[i] = (TW)Ar::val(Ar::ld(ybuf + i));
+  t.sync();
+  mark(ts.log, 14);
 }
 
 // ---------------------------------------------------------------------------

@@ -80,10 +80,13 @@ struct Prob {
   double* partials;
   int kmax;
   gb_step_info* out;
+  PhaseLog log;
   int* flags;  // [0] x0_reset
   // xref (large n): fp64 factors
   const double* LUx;
   const int* permx;
+  const double* xrcph;
+  const double* xrcpl;
   double* rtmp;
   double* dtmp;
 };
@@ -148,7 +151,8 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   using F = Fmt<TW>;
   constexpr int UM = UfMode<TF>::M;
   auto& K = P.K;
-  TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
+  TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch, P.log};
+  mark(ts.log, 30);
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
   int lo, hi;
@@ -195,6 +199,7 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   info.status = st.status;
   info.applies = st.applies;
   info.keff = st.keff;
+  mark(ts.log, 39);
   if (t.leader() && threadIdx.x == 0) {
     *P.out = info;
     *P.epoch = ts.epoch;
@@ -208,7 +213,7 @@ __device__ void xref_refine_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void*
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
-  SysView<TW, double> sx{n, K.sys.lda, K.sys.A, K.sys.lda, P.LUx, P.permx};
+  SysView<TW, double> sx{n, K.sys.lda, K.sys.A, K.sys.lda, P.LUx, P.permx, P.xrcph, P.xrcpl};
   auto* yb = reinterpret_cast<double*>(K.ybuf);
   t.sync();
   op_apply<MODE_F64>(t, sx, (const TW*)nullptr, P.b, P.xref, yb, ts, ops);
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(kThreads) k_lu_small(const TW* A, size_t lda, 
 // ---------------------------------------------------------------------------
 struct SlotLayout {
   size_t stride;
-  size_t A, b, LU, lubuf, perm, xs, r, xref, rtmp, dtmp, V, w, xk, res, s, rhat, C, U, Cn, Un, Ut, Yt, Wd, Qd, H, R,
+  size_t A, b, LU, lubuf, perm, rcph, rcpl, xs, r, xref, rtmp, dtmp, V, w, xk, res, s, rhat, C, U, Cn, Un, Ut, Yt, Wd, Qd, H, R,
       B, bc, dense, gram, ybuf, ctr, epoch, cyc_it, cyc_ke, keff_io, flags, has_xref, out, xa, xb, xyh, xyl, xperm;
 };
 
@@ -439,7 +444,14 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
   K.reorth = B.reorth;
   K.recycling = B.method == METH_GCRODR;
   TW* A = (TW*)(base + Ly.A);
-  K.sys = SysView<TW, TF>{n, (size_t)ldv, A, (size_t)ldv, (const TF*)(base + Ly.LU), (const int*)(base + Ly.perm)};
+  K.sys = SysView<TW, TF>{n,
+                          (size_t)ldv,
+                          A,
+                          (size_t)ldv,
+                          (const TF*)(base + Ly.LU),
+                          (const int*)(base + Ly.perm),
+                          (const double*)(base + Ly.rcph),
+                          (const double*)(base + Ly.rcpl)};
   K.V = (TW*)(base + Ly.V);
   K.w = (TW*)(base + Ly.w);
   K.x = (TW*)(base + Ly.xk);
@@ -539,6 +551,11 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
       }
     }
     um = block_max(um, sm);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      dd q = dd_div(dd{1.0, 0.0}, dd{(double)lub[(size_t)i * n + i], 0.0});
+      ((double*)(base + Ly.rcph))[i] = q.hi;
+      ((double*)(base + Ly.rcpl))[i] = q.lo;
+    }
     __syncthreads();
     int flags = 0;
     if (zero >= 0) {
@@ -666,6 +683,7 @@ struct gb_solver {
   double* stage = nullptr;
   int *perm = nullptr, *piv = nullptr;
   LuStatus* lust = nullptr;
+  double *rcph = nullptr, *rcpl = nullptr, *xrcph = nullptr, *xrcpl = nullptr;
   double *r = nullptr, *xref = nullptr, *rtmp = nullptr, *dtmp = nullptr;
   void *V = nullptr, *w = nullptr, *xk = nullptr, *res = nullptr, *s = nullptr, *rhat = nullptr;
   void *C = nullptr, *U = nullptr, *Cn = nullptr, *Un = nullptr, *Ut = nullptr, *Yt = nullptr;
@@ -674,6 +692,8 @@ struct gb_solver {
   size_t gram_stride = 0;
   void* ybuf = nullptr;
   unsigned long long *ctr = nullptr, *epoch = nullptr, *norms = nullptr;
+  unsigned long long* plog = nullptr;  // phase log (diagnostics), 1 + 2 * cap
+  int plog_cap = 0;
   GridCtl* ctl = nullptr;
   double* partials = nullptr;
   int kmax = 0;
@@ -729,7 +749,8 @@ struct Impl {
     K.tau = s->o.tau;
     K.reorth = s->o.reorthogonalize;
     K.recycling = (s->o.method == GB_RGMRES_IR || s->o.method == GB_RSGMRES_IR);
-    K.sys = SysView<TW, TF>{s->n, (size_t)s->lda, (const TW*)s->A, (size_t)s->lda, (const TF*)s->LU, s->perm};
+    K.sys = SysView<TW, TF>{s->n, (size_t)s->lda, (const TW*)s->A, (size_t)s->lda, (const TF*)s->LU, s->perm,
+                            s->rcph, s->rcpl};
     K.V = (TW*)s->V;
     K.w = (TW*)s->w;
     K.x = (TW*)s->xk;
@@ -779,8 +800,11 @@ struct Impl {
     P.flags = s->flags;
     P.LUx = s->xa;
     P.permx = s->xperm;
+    P.xrcph = s->xrcph;
+    P.xrcpl = s->xrcpl;
     P.rtmp = s->rtmp;
     P.dtmp = s->dtmp;
+    P.log = PhaseLog{s->plog, s->plog_cap};
     return P;
   }
 
@@ -819,6 +843,10 @@ struct Impl {
       s->perm = a.take<int>(ldv);
       s->piv = a.take<int>(64);
       s->lust = a.take<LuStatus>(1);
+      s->rcph = a.take<double>(ldv);
+      s->rcpl = a.take<double>(ldv);
+      s->xrcph = a.take<double>(ldv);
+      s->xrcpl = a.take<double>(ldv);
       s->xs = a.take<TW>(ldv);
       s->r = a.take<double>(ldv);
       s->xref = a.take<double>(ldv);
@@ -909,7 +937,18 @@ struct Impl {
   }
 
   template <int M, class TA, class S>
-  static gb_status lu_run(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st) {
+  static gb_status lu_run(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st,
+                          double* rh, double* rl) {
+    gb_status e = lu_run_core<M>(s, A, lda, W, perm, piv, st);
+    if (e != GB_OK) return e;
+    count_launch();
+    k_lu_rcp<S><<<std::max(1, std::min(1184, (s->n + 255) / 256)), 256, 0, s->stream>>>(W, s->lda, s->n, rh, rl);
+    CK(cudaGetLastError());
+    return GB_OK;
+  }
+
+  template <int M, class TA, class S>
+  static gb_status lu_run_core(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st) {
     const int n = s->n;
     LuStatus init{0x7fffffff, 0, 0ull, 0ull};
     CK(cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
@@ -952,7 +991,8 @@ struct Impl {
 
   static gb_status factor(gb_solver* s, int* zero_col, double* growth) {
     CK(cudaEventRecord(s->ev0, s->stream));
-    gb_status e = lu_run<UM>(s, (const TW*)s->A, (size_t)s->lda, (typename LuT<UM>::S*)s->LU, s->perm, s->piv, s->lust);
+    gb_status e = lu_run<UM>(s, (const TW*)s->A, (size_t)s->lda, (typename LuT<UM>::S*)s->LU, s->perm, s->piv, s->lust,
+                             s->rcph, s->rcpl);
     if (e != GB_OK) return e;
     CK(cudaEventRecord(s->ev1, s->stream));
     LuStatus h;
@@ -987,7 +1027,8 @@ struct Impl {
       CK(cudaGetLastError());
     } else {
       // fp64 GEPP of A (lu_factor(a, DOUBLE)) then the dd-residual refinement
-      gb_status e = lu_run<MODE_F64>(s, (const TW*)s->A, (size_t)s->lda, s->xa, s->xperm, s->xpiv, s->xst);
+      gb_status e = lu_run<MODE_F64>(s, (const TW*)s->A, (size_t)s->lda, s->xa, s->xperm, s->xpiv, s->xst, s->xrcph,
+                                     s->xrcpl);
       if (e != GB_OK) return e;
       LuStatus h;
       CK(cudaMemcpyAsync(&h, s->xst, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
@@ -1092,6 +1133,8 @@ struct Impl {
     Ly.LU = take(sizeof(TF) * (size_t)n * ldv);
     Ly.lubuf = take(sizeof(double) * (size_t)n * n);
     Ly.perm = take(sizeof(int) * ldv);
+    Ly.rcph = take(sizeof(double) * ldv);
+    Ly.rcpl = take(sizeof(double) * ldv);
     Ly.xs = take(sizeof(TW) * ldv);
     Ly.r = take(sizeof(double) * ldv);
     Ly.xref = take(sizeof(double) * ldv);

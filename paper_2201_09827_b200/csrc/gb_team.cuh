@@ -24,6 +24,13 @@ GB_DEVICE unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// relaxed (strong, no L1 invalidation) poll; pair with one fence_acquire()
+GB_DEVICE unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+GB_DEVICE void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 GB_DEVICE void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -66,18 +73,25 @@ struct GridTeam {
 
   __device__ void sync() {
     __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned g = ld_acquire(&ctl->gen);
-      __threadfence();
-      unsigned arrived = atomicAdd(&ctl->count, 1u);
-      if (arrived == (unsigned)G - 1) {
-        atomicExch(&ctl->count, 0u);
-        __threadfence();
-        st_release(&ctl->gen, g + 1);
-      } else {
-        while (ld_acquire(&ctl->gen) == g) __nanosleep(20);
+    if (threadIdx.x < 32) {
+      // the whole warp 0 spins uniformly (a lone spinning lane pays a large
+      // reconvergence penalty on sm_100a, see tools/micro/trsv.cu)
+      unsigned g = 0, last = 0;
+      if (threadIdx.x == 0) {
+        g = ld_relaxed(&ctl->gen);
+        __threadfence();  // release this CTA's writes
+        const unsigned arrived = atomicAdd(&ctl->count, 1u);
+        last = (arrived == (unsigned)G - 1);
+        if (last) {
+          atomicExch(&ctl->count, 0u);
+          st_release(&ctl->gen, g + 1);
+        }
       }
-      __threadfence();
+      g = __shfl_sync(0xffffffffu, g, 0);
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (!last)
+        while (ld_relaxed(&ctl->gen) == g) __nanosleep(16);
+      fence_acq_rel();  // one acquire for everything published before the barrier
     }
     __syncthreads();
   }
