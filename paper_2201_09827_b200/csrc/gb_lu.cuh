@@ -12,6 +12,7 @@
 // Storage: row-major, leading dimension ld.  perm[i] = original row at pivot
 // position i (densela.py:137-140 converts LAPACK ipiv the same way).
 #pragma once
+#include "gb_team.cuh"
 #include "gb_ops.cuh"
 
 namespace gb {
@@ -385,6 +386,304 @@ __global__ void k_lu_umax(const typename LuT<M>::S* W, size_t ld, int n, LuStatu
     }
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) atomic_max_abs(&st->umax_bits, m);
+}
+
+// ---------------------------------------------------------------------------
+// persistent team LU: the whole blocked GEPP in ONE cooperative launch.
+//   per panel of 32 columns:
+//     P  distributed panel factorisation: the panel rows live in the CTAs'
+//        shared memory; per column one grid barrier (candidate pivots and the
+//        candidate rows are staged in global memory, parity double-buffered)
+//     S  row interchanges of the columns outside the panel
+//     T  U12 = L11^-1 A12 (exact per-element order)
+//     G  A22 -= L21 U12 (k applied in order per element; LAPACK modes sum the
+//        32-term block product first, like sgemm/dgemm)
+// ---------------------------------------------------------------------------
+struct LuWork {
+  PivKey* ckey;  // [2][G]
+  double* crow;  // [2][G][32]
+  double* rowk;  // [2][32]
+  int* piv;      // [32]
+};
+
+constexpr int kLuNB = 32;
+
+template <int M>
+__device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, int n, int k0, int i0, int j0,
+                                             typename LuT<M>::C* ls, typename LuT<M>::C* us) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  constexpr int NB = kLuNB, TM = 64, TN = 64;
+  for (int e = threadIdx.x; e < TM * NB; e += blockDim.x) {
+    int r = e / NB, c = e % NB;
+    ls[r * (NB + 1) + c] = (i0 + r < n) ? L::ld(W[(size_t)(i0 + r) * ld + k0 + c]) : C(0);
+  }
+  for (int e = threadIdx.x; e < NB * TN; e += blockDim.x) {
+    int r = e / TN, c = e % TN;
+    us[r * (TN + 1) + c] = (j0 + c < n) ? L::ld(W[(size_t)(k0 + r) * ld + j0 + c]) : C(0);
+  }
+  __syncthreads();
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+  C acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
+      acc[a][b] = (i < n && j < n) ? L::ld(W[(size_t)i * ld + j]) : C(0);
+    }
+  if constexpr (L::kLapack) {
+    C s[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) s[a][b] = C(0);
+#pragma unroll 8
+    for (int k = 0; k < NB; ++k) {
+      C lv[4], uv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) lv[a] = ls[(tr + 16 * a) * (NB + 1) + k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) uv[b] = us[k * (TN + 1) + tc + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] = L::upd(s[a][b], -lv[a], uv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = acc[a][b] - s[a][b];
+  } else {
+#pragma unroll 4
+    for (int k = 0; k < NB; ++k) {
+      C lv[4], uv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) lv[a] = ls[(tr + 16 * a) * (NB + 1) + k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) uv[b] = us[k * (TN + 1) + tc + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = L::upd(acc[a][b], lv[a], uv[b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
+      if (i < n && j < n) W[(size_t)i * ld + j] = L::st(acc[a][b]);
+    }
+  __syncthreads();
+}
+
+template <int M>
+__host__ __device__ inline size_t lu_team_smem(int n, int G) {
+  using C = typename LuT<M>::C;
+  const int sl = (n + G - 1) / G;
+  return sizeof(C) * ((size_t)sl * 33 + 64 + 32 * 33 + 64 * 33 + 32 * 65) + 64;
+}
+
+template <int M, class Team, class TA>
+__device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W, size_t ld, int n, int* perm,
+                        LuStatus* st, LuWork wk, void* smem_raw) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  constexpr int NB = kLuNB;
+  const int G = t.size(), r = t.rank();
+  const int sl_max = (n + G - 1) / G;
+  C* P = reinterpret_cast<C*>(smem_raw);
+  C* pivrow = P + (size_t)sl_max * 33;
+  C* rowkv = pivrow + 32;
+  C* l11 = rowkv + 32;
+  C* ls = l11 + 32 * 33;
+  C* us = ls + 64 * 33;
+  __shared__ PivKey pscr[32];
+  __shared__ int s_p, s_win;
+  __shared__ double s_red[32];
+  const int nthr = G * blockDim.x;
+  const int gtid = r * blockDim.x + threadIdx.x;
+  // W = fl_uf(A), amax, identity permutation
+  {
+    int lo, hi;
+    t.rows(n, lo, hi);
+    double m = 0.0;
+    for (int i = lo; i < hi; ++i)
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        typename L::S s = L::from_u((double)A[(size_t)i * lda + j]);
+        W[(size_t)i * ld + j] = s;
+        const double v = fabs((double)L::ld(s));
+        m = (v > m || v != v) ? v : m;
+      }
+    m = block_max(m, s_red);
+    if (threadIdx.x == 0) atomic_max_abs(&st->amax_bits, m);
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) perm[i] = i;
+  }
+  t.sync();
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    const int kend = min(n, k0 + NB), pw = kend - k0;
+    const int sl = (n - k0 + G - 1) / G;
+    const int p0 = min(n, k0 + r * sl), p1 = min(n, p0 + sl);
+    // ---- P: panel rows into shared memory
+    for (int e = threadIdx.x; e < (p1 - p0) * pw; e += blockDim.x) {
+      const int rr = e / pw, c = e % pw;
+      P[rr * 33 + c] = L::ld(W[(size_t)(p0 + rr) * ld + k0 + c]);
+    }
+    __syncthreads();
+    for (int c = 0; c < pw; ++c) {
+      const int k = k0 + c, par = c & 1;
+      PivKey key{0.0, -1, 0};
+      for (int i = max(p0, k) + threadIdx.x; i < p1; i += blockDim.x) {
+        PivKey cand = make_key((double)P[(i - p0) * 33 + c], i);
+        if (piv_better(cand, key)) key = cand;
+      }
+      key = block_pivot(key, pscr);
+      if (threadIdx.x == 0) wk.ckey[par * G + r] = key;
+      if (key.i >= 0)
+        for (int cc = threadIdx.x; cc < pw; cc += blockDim.x)
+          wk.crow[((size_t)par * G + r) * 32 + cc] = (double)P[(key.i - p0) * 33 + cc];
+      if (k >= p0 && k < p1)
+        for (int cc = threadIdx.x; cc < pw; cc += blockDim.x) wk.rowk[par * 32 + cc] = (double)P[(k - p0) * 33 + cc];
+      t.sync();
+      if (threadIdx.x < 32) {
+        PivKey best{0.0, -1, 0};
+        int bw = -1;
+        for (int g = threadIdx.x; g < G; g += 32) {
+          PivKey q = key;
+          if constexpr (Team::kGrid) {
+            const PivKey* src = wk.ckey + par * G + g;
+            q.v = __ldcg(&src->v);
+            q.i = __ldcg(&src->i);
+            q.nan = __ldcg(&src->nan);
+          }
+          if (piv_better(q, best)) {
+            best = q;
+            bw = g;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          PivKey q = piv_shfl(best, o);
+          int qw = __shfl_xor_sync(0xffffffffu, bw, o);
+          if (piv_better(q, best)) {
+            best = q;
+            bw = qw;
+          }
+        }
+        if (threadIdx.x == 0) {
+          s_p = best.i;
+          s_win = bw;
+        }
+      }
+      __syncthreads();
+      const int p = s_p, win = s_win;
+      for (int cc = threadIdx.x; cc < pw; cc += blockDim.x) {
+        pivrow[cc] = (C)__ldcg(wk.crow + ((size_t)par * G + win) * 32 + cc);
+        rowkv[cc] = (C)__ldcg(wk.rowk + par * 32 + cc);
+      }
+      __syncthreads();
+      const C pv = pivrow[c];
+      const bool isz = (pv == C(0));
+      if (t.leader() && threadIdx.x == 0) {
+        if (isz) atomicMin(&st->zero_col, k);
+        const bool swap = (p != k) && !(isz && L::kLapack);
+        wk.piv[c] = swap ? p : k;
+        if (swap) {
+          int tmp = perm[k];
+          perm[k] = perm[p];
+          perm[p] = tmp;
+        }
+      }
+      if (isz && L::kLapack) {
+        __syncthreads();
+        continue;
+      }
+      if (p != k) {
+        if (p >= p0 && p < p1)
+          for (int cc = threadIdx.x; cc < pw; cc += blockDim.x) P[(p - p0) * 33 + cc] = rowkv[cc];
+        if (k >= p0 && k < p1)
+          for (int cc = threadIdx.x; cc < pw; cc += blockDim.x) P[(k - p0) * 33 + cc] = pivrow[cc];
+      }
+      __syncthreads();
+      for (int i = max(p0, k + 1) + threadIdx.x; i < p1; i += blockDim.x) {
+        C* row = P + (i - p0) * 33;
+        const C lm = L::mult(row[c], pv);
+        row[c] = lm;
+        for (int j = c + 1; j < pw; ++j) row[j] = L::upd(row[j], lm, pivrow[j]);
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < (p1 - p0) * pw; e += blockDim.x) {
+      const int rr = e / pw, c = e % pw;
+      W[(size_t)(p0 + rr) * ld + k0 + c] = L::st(P[rr * 33 + c]);
+    }
+    t.sync();
+    // ---- S: interchanges outside the panel
+    for (int idx = gtid; idx < n - pw; idx += nthr) {
+      const int j = idx < k0 ? idx : idx + pw;
+      for (int c = 0; c < pw; ++c) {
+        const int p = __ldcg(wk.piv + c);
+        if (p != k0 + c) {
+          auto tmp = W[(size_t)(k0 + c) * ld + j];
+          W[(size_t)(k0 + c) * ld + j] = W[(size_t)p * ld + j];
+          W[(size_t)p * ld + j] = tmp;
+        }
+      }
+    }
+    t.sync();
+    if (kend >= n) break;
+    // ---- T: U12 = L11^-1 A12
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+      const int rr = e / NB, c = e % NB;
+      l11[rr * 33 + c] = (rr < pw && c < pw) ? L::ld(W[(size_t)(k0 + rr) * ld + k0 + c]) : C(0);
+    }
+    __syncthreads();
+    for (int j = kend + gtid; j < n; j += nthr) {
+      C col[NB];
+#pragma unroll
+      for (int rr = 0; rr < NB; ++rr) col[rr] = rr < pw ? L::ld(W[(size_t)(k0 + rr) * ld + j]) : C(0);
+#pragma unroll
+      for (int rr = 1; rr < NB; ++rr) {
+#pragma unroll
+        for (int i = 0; i < rr; ++i) col[rr] = L::upd(col[rr], l11[rr * 33 + i], col[i]);
+      }
+#pragma unroll
+      for (int rr = 0; rr < NB; ++rr)
+        if (rr < pw) W[(size_t)(k0 + rr) * ld + j] = L::st(col[rr]);
+    }
+    t.sync();
+    // ---- G: trailing update, 64 x 64 tiles over the team
+    const int rest = n - kend;
+    const int nt = (rest + 63) / 64;
+    for (int tt = r; tt < nt * nt; tt += G) {
+      const int ti = tt / nt, tj = tt % nt;
+      lu_gemm_tile<M>(W, ld, n, k0, kend + ti * 64, kend + tj * 64, ls, us);
+    }
+    t.sync();
+  }
+  // growth numerator max|U| over this CTA's rows
+  {
+    int lo, hi;
+    t.rows(n, lo, hi);
+    double m = 0.0;
+    for (int i = lo; i < hi; ++i)
+      for (int j = i + threadIdx.x; j < n; j += blockDim.x) {
+        const double v = fabs((double)L::ld(W[(size_t)i * ld + j]));
+        m = (v > m || v != v) ? v : m;
+      }
+    m = block_max(m, s_red);
+    if (threadIdx.x == 0) atomic_max_abs(&st->umax_bits, m);
+  }
+}
+
+template <int M, class TA, class Team>
+__global__ void __launch_bounds__(256) k_lu_team(const TA* A, size_t lda, typename LuT<M>::S* W, size_t ld, int n,
+                                                 int* perm, LuStatus* st, LuWork wk, GridCtl* ctl, double* part) {
+  extern __shared__ __align__(16) unsigned char smem_lu[];
+  Team t;
+  if constexpr (Team::kGrid) t = Team{(int)gridDim.x, (int)blockIdx.x, ctl, part, 64, 0u};
+  lu_team<M>(t, A, lda, W, ld, n, perm, st, wk, smem_lu);
 }
 
 }  // namespace gb

@@ -684,6 +684,9 @@ struct gb_solver {
   int *perm = nullptr, *piv = nullptr;
   LuStatus* lust = nullptr;
   double *rcph = nullptr, *rcpl = nullptr, *xrcph = nullptr, *xrcpl = nullptr;
+  PivKey* lu_ckey = nullptr;
+  double *lu_crow = nullptr, *lu_rowk = nullptr;
+  int* lu_piv = nullptr;
   double *r = nullptr, *xref = nullptr, *rtmp = nullptr, *dtmp = nullptr;
   void *V = nullptr, *w = nullptr, *xk = nullptr, *res = nullptr, *s = nullptr, *rhat = nullptr;
   void *C = nullptr, *U = nullptr, *Cn = nullptr, *Un = nullptr, *Ut = nullptr, *Yt = nullptr;
@@ -843,6 +846,10 @@ struct Impl {
       s->perm = a.take<int>(ldv);
       s->piv = a.take<int>(64);
       s->lust = a.take<LuStatus>(1);
+      s->lu_ckey = a.take<PivKey>(2 * 160);
+      s->lu_crow = a.take<double>(2 * 160 * 32);
+      s->lu_rowk = a.take<double>(64);
+      s->lu_piv = a.take<int>(64);
       s->rcph = a.take<double>(ldv);
       s->rcpl = a.take<double>(ldv);
       s->xrcph = a.take<double>(ldv);
@@ -952,7 +959,7 @@ struct Impl {
     const int n = s->n;
     LuStatus init{0x7fffffff, 0, 0ull, 0ull};
     CK(cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
-    if (n <= 128 && M != MODE_F64) {
+    if (n <= 128 && M == MODE_H16) {
       size_t sm = (size_t)n * n * sizeof(typename LuT<M>::C);
       gb_status e = set_smem(k_lu_small<M, TA>, sm);
       if (e != GB_OK) return e;
@@ -961,31 +968,32 @@ struct Impl {
       CK(cudaGetLastError());
       return GB_OK;
     }
-    constexpr int NB = 32;
+    // one persistent cooperative launch for the whole blocked factorisation
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int G = n <= 256 ? 1 : std::min(sms, (n + 63) / 64);
+    const size_t smb = lu_team_smem<M>(n, G);
+    LuWork wk{s->lu_ckey, s->lu_crow, s->lu_rowk, s->lu_piv};
     count_launch();
-    k_lu_convert<M, TA><<<1184, 256, 0, s->stream>>>(A, lda, W, s->lda, n, st);
-    CK(cudaGetLastError());
-    // identity permutation
-    std::vector<int> id(n);
-    for (int i = 0; i < n; ++i) id[i] = i;
-    CK(cudaMemcpyAsync(perm, id.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
-    for (int k0 = 0; k0 < n; k0 += NB) {
-      count_launch(1 + (n - std::min(NB, n - k0) > 0) + 2 * (n - (k0 + NB) > 0));
-      k_lu_panel<M><<<1, 1024, 0, s->stream>>>(W, s->lda, n, k0, NB, perm, piv, st);
-      int outside = n - std::min(NB, n - k0);
-      if (outside > 0) k_lu_laswp<M><<<(outside + 255) / 256, 256, 0, s->stream>>>(W, s->lda, n, k0, NB, piv);
-      int rest = n - (k0 + NB);
-      if (rest > 0) {
-        k_lu_trsm<M, NB><<<std::min(1184, (rest + 127) / 128), 128, 0, s->stream>>>(W, s->lda, n, k0);
-        dim3 g((rest + 63) / 64, (rest + 63) / 64);
-        k_lu_gemm<M, NB><<<g, 256, 0, s->stream>>>(W, s->lda, n, k0);
-      }
+    if (G == 1) {
+      auto kern = k_lu_team<M, TA, CtaTeam>;
+      gb_status e = set_smem(kern, smb);
+      if (e != GB_OK) return e;
+      kern<<<1, 256, smb, s->stream>>>(A, lda, W, (size_t)s->lda, n, perm, st, wk, s->ctl, s->partials);
+      CK(cudaGetLastError());
+    } else {
+      auto kern = k_lu_team<M, TA, GridTeam>;
+      gb_status e = set_smem(kern, smb);
+      if (e != GB_OK) return e;
+      size_t ldw = (size_t)s->lda;
+      GridCtl* ctl = s->ctl;
+      double* part = s->partials;
+      void* argv[] = {(void*)&A, (void*)&lda, (void*)&W, (void*)&ldw, (void*)&n, (void*)&perm, (void*)&st,
+                      (void*)&wk, (void*)&ctl, (void*)&part};
+      CK(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(256), argv, smb, s->stream));
     }
-    CK(cudaGetLastError());
-    count_launch();
-    k_lu_umax<M><<<std::min(n, 1184), 256, 0, s->stream>>>(W, s->lda, n, st);
-    CK(cudaGetLastError());
+    (void)piv;
     return GB_OK;
   }
 
