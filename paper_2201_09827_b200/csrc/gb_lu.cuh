@@ -374,6 +374,55 @@ __global__ void k_lu_rcp(const S* W, size_t ld, int n, double* rh, double* rl) {
   }
 }
 
+// dd-accurate inverses of the 32x32 diagonal blocks (for the non-exact
+// substitution modes): one warp per block, lane c builds column c.
+// Layout: element (i, j) of block b at b*1024 + j*32 + i; L part strictly
+// lower (unit diagonal implied), U part upper including the diagonal.
+template <class S>
+__device__ void diag_inv_block(const S* W, size_t ld, int n, int b, double* lh, double* ll, double* uh,
+                               double* ul) {
+  const int c = threadIdx.x & 31;
+  const int r0 = b * 32;
+  const int m = min(32, n - r0);
+  dd x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = dd{0.0, 0.0};
+  if (c < m) {
+    x[c] = dd{1.0, 0.0};
+    for (int i = c + 1; i < m; ++i) {
+      dd s{0.0, 0.0};
+      for (int j = c; j < i; ++j) s = dd_add(s, dd_scale(to_d(W[(size_t)(r0 + i) * ld + r0 + j]), x[j]));
+      x[i] = dd_neg(s);
+    }
+  }
+  for (int i = 0; i < 32; ++i) {
+    lh[(size_t)b * 1024 + c * 32 + i] = (i > c && c < m) ? x[i].hi : 0.0;
+    ll[(size_t)b * 1024 + c * 32 + i] = (i > c && c < m) ? x[i].lo : 0.0;
+    x[i] = dd{0.0, 0.0};
+  }
+  if (c < m) {
+    x[c] = dd_div(dd{1.0, 0.0}, dd{to_d(W[(size_t)(r0 + c) * ld + r0 + c]), 0.0});
+    for (int i = c - 1; i >= 0; --i) {
+      dd s{0.0, 0.0};
+      for (int j = i + 1; j <= c; ++j) s = dd_add(s, dd_scale(to_d(W[(size_t)(r0 + i) * ld + r0 + j]), x[j]));
+      const dd ri = dd_div(dd{1.0, 0.0}, dd{to_d(W[(size_t)(r0 + i) * ld + r0 + i]), 0.0});
+      x[i] = dd_neg(dd_mul(s, ri));
+    }
+  }
+  for (int i = 0; i < 32; ++i) {
+    uh[(size_t)b * 1024 + c * 32 + i] = (i <= c && c < m) ? x[i].hi : 0.0;
+    ul[(size_t)b * 1024 + c * 32 + i] = (i <= c && c < m) ? x[i].lo : 0.0;
+  }
+}
+
+template <class S>
+__global__ void k_diag_inv(const S* W, size_t ld, int n, double* lh, double* ll, double* uh, double* ul) {
+  const int wpb = blockDim.x / 32;
+  const int nb = (n + 31) / 32;
+  for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < nb; b += gridDim.x * wpb)
+    diag_inv_block(W, ld, n, b, lh, ll, uh, ul);
+}
+
 // max |U| over the upper triangle
 template <int M>
 __global__ void k_lu_umax(const typename LuT<M>::S* W, size_t ld, int n, LuStatus* st) {

@@ -53,6 +53,9 @@ struct Arith<MODE_F64> {
   GB_DEVICE static T sub(T a, T b) { return __dsub_rn(a, b); }
   GB_DEVICE static T div(T y, double u) { return __ddiv_rn(y, u); }
   GB_DEVICE static T mul_rcp(T y, double rh, double) { return __dmul_rn(y, rh); }
+  GB_DEVICE static T mac_t(T s, double l, T y) { return __fma_rn(l, y, s); }
+  GB_DEVICE static T mac_inv(T s, double ih, double, T t) { return __fma_rn(ih, t, s); }
+  static constexpr bool kInv = true;
   GB_DEVICE static double val(T x) { return x; }
   GB_DEVICE static T shfl(T x, int src) { return __shfl_sync(0xffffffffu, x, src); }
   GB_DEVICE static T ld(const T* p) { return __ldcg(p); }
@@ -70,6 +73,9 @@ struct Arith<MODE_F32> {
   GB_DEVICE static T sub(T a, T b) { return __fsub_rn(a, b); }
   GB_DEVICE static T div(T y, double u) { return __fdiv_rn(y, (float)u); }
   GB_DEVICE static T mul_rcp(T y, double rh, double) { return __fmul_rn(y, (float)rh); }
+  GB_DEVICE static T mac_t(T s, double l, T y) { return __fmaf_rn((float)l, y, s); }
+  GB_DEVICE static T mac_inv(T s, double ih, double, T t) { return s; }
+  static constexpr bool kInv = false;
   GB_DEVICE static double val(T x) { return (double)x; }
   GB_DEVICE static T shfl(T x, int src) { return __shfl_sync(0xffffffffu, x, src); }
   GB_DEVICE static T ld(const T* p) { return __ldcg(p); }
@@ -88,6 +94,9 @@ struct Arith<MODE_H16> {
   GB_DEVICE static T sub(T a, T b) { return h_sub(a, b); }
   GB_DEVICE static T div(T y, double u) { return h_div(y, (float)u); }
   GB_DEVICE static T mul_rcp(T y, double, double) { return y; }  // never used (exact order)
+  GB_DEVICE static T mac_t(T s, double, T) { return s; }           // never used (exact order)
+  GB_DEVICE static T mac_inv(T s, double, double, T) { return s; }
+  static constexpr bool kInv = false;
   GB_DEVICE static double val(T x) { return (double)x; }
   GB_DEVICE static T shfl(T x, int src) { return __shfl_sync(0xffffffffu, x, src); }
   GB_DEVICE static T ld(const T* p) { return __ldcg(p); }
@@ -105,6 +114,9 @@ struct Arith<MODE_DD> {
   GB_DEVICE static T sub(T a, T b) { return dd_sub(a, b); }
   GB_DEVICE static T div(T y, double u) { return dd_div(y, dd{u, 0.0}); }
   GB_DEVICE static T mul_rcp(T y, double rh, double rl) { return dd_mul(y, dd{rh, rl}); }
+  GB_DEVICE static T mac_t(T s, double l, T y) { return dd_add(s, dd_scale(l, y)); }
+  GB_DEVICE static T mac_inv(T s, double ih, double il, T t) { return dd_add(s, dd_mul(dd{ih, il}, t)); }
+  static constexpr bool kInv = true;
   GB_DEVICE static double val(T x) { return dd_val(x); }
   GB_DEVICE static T shfl(T x, int src) {
     return dd{__shfl_sync(0xffffffffu, x.hi, src), __shfl_sync(0xffffffffu, x.lo, src)};
@@ -145,6 +157,13 @@ struct SysView {
   // keep divisions off the substitution's critical path; nullptr -> divide
   const double* rcp_hi;
   const double* rcp_lo;
+  // dd-accurate inverses of the 32x32 diagonal blocks of L (strictly lower
+  // part, unit diagonal implied) and U; element (i, j) of block b at
+  // b*1024 + j*32 + i.  nullptr -> sequential substitution.
+  const double* linv_hi;
+  const double* linv_lo;
+  const double* uinv_hi;
+  const double* uinv_lo;
 };
 
 // progress counters of the flag-based TRSV (one per direction)
@@ -234,7 +253,8 @@ GB_DEVICE void wait_ctr(unsigned long long* gctr, volatile unsigned long long* s
 template <int M, class Team, class TF, bool kLower>
 __device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename Arith<M>::T* y,
                             const TrsvSync& ts, void* smem_raw, const double* rcph = nullptr,
-                            const double* rcpl = nullptr) {
+                            const double* rcpl = nullptr, const double* inv_h = nullptr,
+                            const double* inv_l = nullptr) {
   using Ar = Arith<M>;
   using T = typename Ar::T;
   using TT = typename TileT<TF>::T;
@@ -282,9 +302,20 @@ __device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename A
       if (ts.stamps != nullptr && lane == 0 && q + 1 == noff) ts.stamps[3 * s + 2] = gtimer();
       __syncwarp();
       const T yv = (c0 + lane < n) ? Ar::ld(y + c0 + lane) : Ar::zero();
-      if (kLower) {
-        // branch-free: divergence inside these loops costs a warp
-        // reconvergence per step on sm_100a
+      if constexpr (!Ar::kExactOrder) {
+        // four independent partial sums (entries beyond n are zero)
+        T s0 = Ar::zero(), s1 = Ar::zero(), s2 = Ar::zero(), s3 = Ar::zero();
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          s0 = Ar::mac_t(s0, (double)tile[lane * 33 + jj], Ar::shfl(yv, jj));
+          s1 = Ar::mac_t(s1, (double)tile[lane * 33 + jj + 1], Ar::shfl(yv, jj + 1));
+          s2 = Ar::mac_t(s2, (double)tile[lane * 33 + jj + 2], Ar::shfl(yv, jj + 2));
+          s3 = Ar::mac_t(s3, (double)tile[lane * 33 + jj + 3], Ar::shfl(yv, jj + 3));
+        }
+        acc = Ar::sub(acc, Ar::add(Ar::add(s0, s1), Ar::add(s2, s3)));
+      } else if (kLower) {
+        // exact column-sweep order, branch-free: divergence inside these
+        // loops costs a warp reconvergence per step on sm_100a
 #pragma unroll 8
         for (int jj = 0; jj < 32; ++jj) {
           const T yj = Ar::shfl(yv, jj);
@@ -299,6 +330,27 @@ __device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename A
       }
     }
     if (ts.stamps != nullptr && lane == 0) ts.stamps[3 * s] = gtimer();
+    if constexpr (Ar::kInv) {
+      if (inv_h != nullptr) {
+        // y_b = inv(D_b) t_b as a 32-term dot per lane (no sequential chain);
+        // lower: unit diagonal implied (strictly lower part stored)
+        const double* ih = inv_h + (size_t)b * 1024 + lane;
+        const double* il = inv_l != nullptr ? inv_l + (size_t)b * 1024 + lane : nullptr;
+        T s0 = kLower ? acc : Ar::zero(), s1 = Ar::zero(), s2 = Ar::zero(), s3 = Ar::zero();
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          const T t0 = Ar::shfl(acc, jj), t1 = Ar::shfl(acc, jj + 1), t2 = Ar::shfl(acc, jj + 2),
+                  t3 = Ar::shfl(acc, jj + 3);
+          s0 = Ar::mac_inv(s0, __ldg(ih + (jj)*32), il ? __ldg(il + (jj)*32) : 0.0, t0);
+          s1 = Ar::mac_inv(s1, __ldg(ih + (jj + 1) * 32), il ? __ldg(il + (jj + 1) * 32) : 0.0, t1);
+          s2 = Ar::mac_inv(s2, __ldg(ih + (jj + 2) * 32), il ? __ldg(il + (jj + 2) * 32) : 0.0, t2);
+          s3 = Ar::mac_inv(s3, __ldg(ih + (jj + 3) * 32), il ? __ldg(il + (jj + 3) * 32) : 0.0, t3);
+        }
+        acc = Ar::add(Ar::add(s0, s1), Ar::add(s2, s3));
+        if (rv) y[row] = acc;
+        goto published;
+      }
+    }
     // diagonal block (its tile is already in v)
     __syncwarp();
     tile_store(tile, v);
@@ -323,8 +375,9 @@ __device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename A
         acc = sel(lane < jj && row0 + jj < n, Ar::sub_prod(acc, (double)tile[lane * 33 + jj], yj), acc);
       }
     }
-    if (ts.stamps != nullptr && lane == 0) ts.stamps[3 * s + 1] = gtimer();
     if (rv) y[row] = acc;
+  published:
+    if (ts.stamps != nullptr && lane == 0) ts.stamps[3 * s + 1] = gtimer();
     __syncwarp();
     if (lane == 0) {
       if constexpr (Team::kGrid) {
@@ -451,9 +504,9 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
   t.sync();
   mark(ts.log, 11);
   // 2. forward (unit lower) then backward (upper)
-  trsv_blocks<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem);
+  trsv_blocks<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, nullptr, nullptr, s.linv_hi, s.linv_lo);
   mark(ts.log, 12);
-  trsv_blocks<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.rcp_hi, s.rcp_lo);
+  trsv_blocks<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.rcp_hi, s.rcp_lo, s.uinv_hi, s.uinv_lo);
   mark(ts.log, 13);
   ts.epoch++;
   // 3. round to u (rows of this CTA's slice; the backward sweep is complete

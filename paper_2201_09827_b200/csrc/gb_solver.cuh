@@ -87,6 +87,7 @@ struct Prob {
   const int* permx;
   const double* xrcph;
   const double* xrcpl;
+  const double *xlinvh, *xlinvl, *xuinvh, *xuinvl;
   double* rtmp;
   double* dtmp;
 };
@@ -213,7 +214,8 @@ __device__ void xref_refine_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void*
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
-  SysView<TW, double> sx{n, K.sys.lda, K.sys.A, K.sys.lda, P.LUx, P.permx, P.xrcph, P.xrcpl};
+  SysView<TW, double> sx{n,       K.sys.lda, K.sys.A,  K.sys.lda, P.LUx,    P.permx,
+                         P.xrcph, P.xrcpl,   P.xlinvh, P.xlinvl,  P.xuinvh, P.xuinvl};
   auto* yb = reinterpret_cast<double*>(K.ybuf);
   t.sync();
   op_apply<MODE_F64>(t, sx, (const TW*)nullptr, P.b, P.xref, yb, ts, ops);
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(kThreads) k_lu_small(const TW* A, size_t lda, 
 // ---------------------------------------------------------------------------
 struct SlotLayout {
   size_t stride;
-  size_t A, b, LU, lubuf, perm, rcph, rcpl, xs, r, xref, rtmp, dtmp, V, w, xk, res, s, rhat, C, U, Cn, Un, Ut, Yt, Wd, Qd, H, R,
+  size_t A, b, LU, lubuf, perm, rcph, rcpl, linvh, linvl, uinvh, uinvl, xs, r, xref, rtmp, dtmp, V, w, xk, res, s, rhat, C, U, Cn, Un, Ut, Yt, Wd, Qd, H, R,
       B, bc, dense, gram, ybuf, ctr, epoch, cyc_it, cyc_ke, keff_io, flags, has_xref, out, xa, xb, xyh, xyl, xperm;
 };
 
@@ -451,7 +453,11 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
                           (const TF*)(base + Ly.LU),
                           (const int*)(base + Ly.perm),
                           (const double*)(base + Ly.rcph),
-                          (const double*)(base + Ly.rcpl)};
+                          (const double*)(base + Ly.rcpl),
+                          (const double*)(base + Ly.linvh),
+                          (const double*)(base + Ly.linvl),
+                          (const double*)(base + Ly.uinvh),
+                          (const double*)(base + Ly.uinvl)};
   K.V = (TW*)(base + Ly.V);
   K.w = (TW*)(base + Ly.w);
   K.x = (TW*)(base + Ly.xk);
@@ -556,6 +562,10 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
       ((double*)(base + Ly.rcph))[i] = q.hi;
       ((double*)(base + Ly.rcpl))[i] = q.lo;
     }
+    __syncthreads();
+    for (int bk = threadIdx.x >> 5; bk < (n + 31) / 32; bk += blockDim.x >> 5)
+      diag_inv_block(LUo, (size_t)ldv, n, bk, (double*)(base + Ly.linvh), (double*)(base + Ly.linvl),
+                     (double*)(base + Ly.uinvh), (double*)(base + Ly.uinvl));
     __syncthreads();
     int flags = 0;
     if (zero >= 0) {
@@ -684,6 +694,8 @@ struct gb_solver {
   int *perm = nullptr, *piv = nullptr;
   LuStatus* lust = nullptr;
   double *rcph = nullptr, *rcpl = nullptr, *xrcph = nullptr, *xrcpl = nullptr;
+  double *linvh = nullptr, *linvl = nullptr, *uinvh = nullptr, *uinvl = nullptr;
+  double *xlinvh = nullptr, *xlinvl = nullptr, *xuinvh = nullptr, *xuinvl = nullptr;
   PivKey* lu_ckey = nullptr;
   double *lu_crow = nullptr, *lu_rowk = nullptr;
   int* lu_piv = nullptr;
@@ -752,8 +764,8 @@ struct Impl {
     K.tau = s->o.tau;
     K.reorth = s->o.reorthogonalize;
     K.recycling = (s->o.method == GB_RGMRES_IR || s->o.method == GB_RSGMRES_IR);
-    K.sys = SysView<TW, TF>{s->n, (size_t)s->lda, (const TW*)s->A, (size_t)s->lda, (const TF*)s->LU, s->perm,
-                            s->rcph, s->rcpl};
+    K.sys = SysView<TW, TF>{s->n,     (size_t)s->lda, (const TW*)s->A, (size_t)s->lda, (const TF*)s->LU, s->perm,
+                            s->rcph,  s->rcpl,        s->linvh,        s->linvl,        s->uinvh,          s->uinvl};
     K.V = (TW*)s->V;
     K.w = (TW*)s->w;
     K.x = (TW*)s->xk;
@@ -805,6 +817,10 @@ struct Impl {
     P.permx = s->xperm;
     P.xrcph = s->xrcph;
     P.xrcpl = s->xrcpl;
+    P.xlinvh = s->xlinvh;
+    P.xlinvl = s->xlinvl;
+    P.xuinvh = s->xuinvh;
+    P.xuinvl = s->xuinvl;
     P.rtmp = s->rtmp;
     P.dtmp = s->dtmp;
     P.log = PhaseLog{s->plog, s->plog_cap};
@@ -846,6 +862,15 @@ struct Impl {
       s->perm = a.take<int>(ldv);
       s->piv = a.take<int>(64);
       s->lust = a.take<LuStatus>(1);
+      const size_t ninv = (size_t)((n + 31) / 32) * 1024;
+      s->linvh = a.take<double>(ninv);
+      s->linvl = a.take<double>(ninv);
+      s->uinvh = a.take<double>(ninv);
+      s->uinvl = a.take<double>(ninv);
+      s->xlinvh = a.take<double>(ninv);
+      s->xlinvl = a.take<double>(ninv);
+      s->xuinvh = a.take<double>(ninv);
+      s->xuinvl = a.take<double>(ninv);
       s->lu_ckey = a.take<PivKey>(2 * 160);
       s->lu_crow = a.take<double>(2 * 160 * 32);
       s->lu_rowk = a.take<double>(64);
@@ -945,11 +970,13 @@ struct Impl {
 
   template <int M, class TA, class S>
   static gb_status lu_run(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st,
-                          double* rh, double* rl) {
+                          double* rh, double* rl, double* ilh, double* ill, double* iuh, double* iul) {
     gb_status e = lu_run_core<M>(s, A, lda, W, perm, piv, st);
     if (e != GB_OK) return e;
-    count_launch();
+    count_launch(2);
     k_lu_rcp<S><<<std::max(1, std::min(1184, (s->n + 255) / 256)), 256, 0, s->stream>>>(W, s->lda, s->n, rh, rl);
+    const int nbk = (s->n + 31) / 32;
+    k_diag_inv<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
     CK(cudaGetLastError());
     return GB_OK;
   }
@@ -1000,7 +1027,7 @@ struct Impl {
   static gb_status factor(gb_solver* s, int* zero_col, double* growth) {
     CK(cudaEventRecord(s->ev0, s->stream));
     gb_status e = lu_run<UM>(s, (const TW*)s->A, (size_t)s->lda, (typename LuT<UM>::S*)s->LU, s->perm, s->piv, s->lust,
-                             s->rcph, s->rcpl);
+                             s->rcph, s->rcpl, s->linvh, s->linvl, s->uinvh, s->uinvl);
     if (e != GB_OK) return e;
     CK(cudaEventRecord(s->ev1, s->stream));
     LuStatus h;
@@ -1036,7 +1063,7 @@ struct Impl {
     } else {
       // fp64 GEPP of A (lu_factor(a, DOUBLE)) then the dd-residual refinement
       gb_status e = lu_run<MODE_F64>(s, (const TW*)s->A, (size_t)s->lda, s->xa, s->xperm, s->xpiv, s->xst, s->xrcph,
-                                     s->xrcpl);
+                                     s->xrcpl, s->xlinvh, s->xlinvl, s->xuinvh, s->xuinvl);
       if (e != GB_OK) return e;
       LuStatus h;
       CK(cudaMemcpyAsync(&h, s->xst, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
@@ -1143,6 +1170,10 @@ struct Impl {
     Ly.perm = take(sizeof(int) * ldv);
     Ly.rcph = take(sizeof(double) * ldv);
     Ly.rcpl = take(sizeof(double) * ldv);
+    Ly.linvh = take(sizeof(double) * (size_t)ldv * 32);
+    Ly.linvl = take(sizeof(double) * (size_t)ldv * 32);
+    Ly.uinvh = take(sizeof(double) * (size_t)ldv * 32);
+    Ly.uinvl = take(sizeof(double) * (size_t)ldv * 32);
     Ly.xs = take(sizeof(TW) * ldv);
     Ly.r = take(sizeof(double) * ldv);
     Ly.xref = take(sizeof(double) * ldv);

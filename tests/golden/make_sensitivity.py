@@ -125,8 +125,26 @@ def envelope(a, b, prec, method, m, k, tau, i_max):
             "verdicts": sorted({(r["converged"], r["reason"] or "") for r in runs.values()})}
 
 
+def lu_divergence(a, uf="single"):
+    """First pivot index where a different valid GEPP (unblocked, no FMA)
+    departs from the reference's LAPACK factorisation; None if never."""
+    au = O.rnd(np.asarray(a, dtype=np.float64), O.DOUBLE)
+    ref = _orig["lu_factor"](au, uf)
+    alt = lu_unblocked(au, uf)
+    d = np.nonzero(ref.perm != alt.perm)[0]
+    return int(d[0]) if d.size else None
+
+
+def main_lu(out):
+    lu = json.load(open(os.path.join(HERE, "lu.json")))
+    z = np.load(os.path.join(HERE, "lu.npz"))
+    out["lu"] = {name: lu_divergence(z[f"{name}_a"], meta["uf"])
+                 for name, meta in lu.items() if meta.get("uf") == "single" and f"{name}_a" in z}
+
+
 def main():
     out = {"tables": [], "cfg1": {}, "cfg3": []}
+    main_lu(out)
     for tab in ("table5", "table6"):
         for row in json.load(open(os.path.join(HERE, f"{tab}.json")))["rows"]:
             a = problems.prolate(100, row["alpha"])
@@ -154,4 +172,10 @@ def main():
 if __name__ == "__main__":
     if os.environ.get("OPENBLAS_NUM_THREADS") != "1":
         sys.exit("set OPENBLAS_NUM_THREADS=1")
-    main()
+    if "--lu-only" in sys.argv:
+        path = os.path.join(HERE, "sensitivity.json")
+        data = json.load(open(path))
+        main_lu(data)
+        json.dump(data, open(path, "w"), indent=0)
+    else:
+        main()
