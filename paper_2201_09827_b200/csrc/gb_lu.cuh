@@ -14,6 +14,7 @@
 #pragma once
 #include "gb_team.cuh"
 #include "gb_ops.cuh"
+#include "gb_tc.cuh"
 
 namespace gb {
 
@@ -531,12 +532,85 @@ template <int M>
 __host__ __device__ inline size_t lu_team_smem(int n, int G) {
   using C = typename LuT<M>::C;
   const int sl = (n + G - 1) / G;
-  return sizeof(C) * ((size_t)sl * 33 + 64 + 32 * 33 + 64 * 33 + 32 * 65) + 64;
+  const size_t simt = sizeof(C) * ((size_t)sl * 33 + 64 + 32 * 33 + 64 * 33 + 32 * 65) + 64;
+  // tensor-core tiles (A 128x32, B 256x32 fp16, 1024-B aligned) + barrier
+  return ((simt + 1023) & ~(size_t)1023) + 8192 + 16384 + 64;
+}
+
+// ---------------------------------------------------------------------------
+// tensor-core mode of the fp16 trailing update (lu_mode = 1):
+//   A22[i0:i0+128, j0:j0+256] = fl16(A22 - L21 U12) with the 32-wide panel
+//   product on tcgen05 (fp16 operands, fp32 accumulator in TMEM).  Results are
+//   rounded to u_f once per panel (north_star (1)); pivots then agree with the
+//   exact mode up to near-ties.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, int i0, int j0, unsigned char* sA,
+                                           unsigned char* sB, uint64_t* mbar, uint32_t tmem, uint32_t& phase) {
+  // A: L21 rows [i0, i0+128), panel columns [k0, k0+32): K-major already
+  for (int e = threadIdx.x; e < 128 * 4; e += blockDim.x) {
+    const int r = e >> 2, c = e & 3;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    const int gi = i0 + r;
+    if (gi < n) v = *reinterpret_cast<const uint4*>(W + (size_t)gi * ld + k0 + c * 8);
+    *reinterpret_cast<uint4*>(sA + tc::sw64_off(r, c * 8)) = v;
+  }
+  // B: U12 rows [k0, k0+32), columns [j0, j0+256) transposed to K-major
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int k = e >> 5, cj = e & 31;
+    const int gj = j0 + cj * 8;
+    __align__(16) __half h[8];
+    if (gj + 8 <= n) {
+      *reinterpret_cast<uint4*>(h) = *reinterpret_cast<const uint4*>(W + (size_t)(k0 + k) * ld + gj);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = (gj + q < n) ? W[(size_t)(k0 + k) * ld + gj + q] : __float2half(0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) *reinterpret_cast<__half*>(sB + tc::sw64_off(cj * 8 + q, k)) = h[q];
+  }
+  tc::fence_proxy_async();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc::fence_after();
+    constexpr uint32_t idesc = tc::idesc_f16_f32(128, 256);
+    const uint64_t ad = tc::desc_k64(tc::smem_u32(sA)), bd = tc::desc_k64(tc::smem_u32(sB));
+    tc::mma_f16(tmem, ad, bd, idesc, 0u);
+    tc::mma_f16(tmem, ad + 2, bd + 2, idesc, 1u);  // K = 16..31: +32 bytes inside the swizzle atom
+    tc::commit(mbar);
+  }
+  tc::mbar_wait(mbar, phase);
+  phase ^= 1u;
+  tc::fence_after();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = (w & 3) * 32 + lane, gi = i0 + row;
+  const int cbase = (w >> 2) * 128;
+#pragma unroll 1
+  for (int ch = 0; ch < 4; ++ch) {
+    float acc[32];
+    tc::tmem_ld32(tmem + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)(cbase + ch * 32), acc);
+    const int gj = j0 + cbase + ch * 32;
+    if (gi < n && gj < n) {
+      __half* p = W + (size_t)gi * ld + gj;
+      if (gj + 32 <= n) {
+        __align__(16) __half h[32];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(h)[q] = reinterpret_cast<const uint4*>(p)[q];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) h[q] = __float2half_rn(__half2float(h[q]) - acc[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(p)[q] = reinterpret_cast<const uint4*>(h)[q];
+      } else {
+        for (int q = 0; q < 32 && gj + q < n; ++q) p[q] = __float2half_rn(__half2float(p[q]) - acc[q]);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
 }
 
 template <int M, class Team, class TA>
 __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W, size_t ld, int n, int* perm,
-                        LuStatus* st, LuWork wk, void* smem_raw) {
+                        LuStatus* st, LuWork wk, void* smem_raw, int tcmode = 0) {
   using L = LuT<M>;
   using C = typename L::C;
   constexpr int NB = kLuNB;
@@ -551,6 +625,23 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
   __shared__ PivKey pscr[32];
   __shared__ int s_p, s_win;
   __shared__ double s_red[32];
+  __shared__ uint32_t s_tmem;
+  // tensor-core staging (TC mode, fp16 only)
+  const size_t simt_bytes = sizeof(C) * ((size_t)sl_max * 33 + 64 + 32 * 33 + 64 * 33 + 32 * 65) + 64;
+  unsigned char* tcbase = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + ((simt_bytes + 1023) & ~(size_t)1023) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = tcbase;
+  unsigned char* sB = tcbase + 8192;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tcbase + 8192 + 16384);
+  const bool use_tc = (M == MODE_H16) && tcmode != 0;
+  uint32_t tphase = 0;
+  if (use_tc) {
+    if (threadIdx.x < 32) tc::tmem_alloc(&s_tmem, 256);
+    if (threadIdx.x == 0) tc::mbar_init(mbar, 1);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
   const int nthr = G * blockDim.x;
   const int gtid = r * blockDim.x + threadIdx.x;
   // W = fl_uf(A), amax, identity permutation
@@ -702,14 +793,29 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
         if (rr < pw) W[(size_t)(k0 + rr) * ld + j] = L::st(col[rr]);
     }
     t.sync();
-    // ---- G: trailing update, 64 x 64 tiles over the team
+    // ---- G: trailing update over the team
     const int rest = n - kend;
+    if constexpr (M == MODE_H16) {
+      if (use_tc && pw == NB) {
+        const int ntr = (rest + 127) / 128, ntc = (rest + 255) / 256;
+        for (int tt = r; tt < ntr * ntc; tt += G)
+          lu_tc_tile(reinterpret_cast<__half*>(W), ld, n, k0, kend + (tt / ntc) * 128, kend + (tt % ntc) * 256, sA,
+                     sB, mbar, s_tmem, tphase);
+        t.sync();
+        continue;
+      }
+    }
     const int nt = (rest + 63) / 64;
     for (int tt = r; tt < nt * nt; tt += G) {
       const int ti = tt / nt, tj = tt % nt;
       lu_gemm_tile<M>(W, ld, n, k0, kend + ti * 64, kend + tj * 64, ls, us);
     }
     t.sync();
+  }
+  if (use_tc) {
+    tc::fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tc::tmem_dealloc(s_tmem, 256);
   }
   // growth numerator max|U| over this CTA's rows
   {
@@ -728,11 +834,12 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
 
 template <int M, class TA, class Team>
 __global__ void __launch_bounds__(256) k_lu_team(const TA* A, size_t lda, typename LuT<M>::S* W, size_t ld, int n,
-                                                 int* perm, LuStatus* st, LuWork wk, GridCtl* ctl, double* part) {
-  extern __shared__ __align__(16) unsigned char smem_lu[];
+                                                 int* perm, LuStatus* st, LuWork wk, GridCtl* ctl, double* part,
+                                                 int tcmode) {
+  extern __shared__ __align__(1024) unsigned char smem_lu[];
   Team t;
   if constexpr (Team::kGrid) t = Team{(int)gridDim.x, (int)blockIdx.x, ctl, part, 64, 0u};
-  lu_team<M>(t, A, lda, W, ld, n, perm, st, wk, smem_lu);
+  lu_team<M>(t, A, lda, W, ld, n, perm, st, wk, smem_lu, tcmode);
 }
 
 }  // namespace gb

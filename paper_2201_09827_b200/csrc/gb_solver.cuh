@@ -970,8 +970,9 @@ struct Impl {
 
   template <int M, class TA, class S>
   static gb_status lu_run(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st,
-                          double* rh, double* rl, double* ilh, double* ill, double* iuh, double* iul) {
-    gb_status e = lu_run_core<M>(s, A, lda, W, perm, piv, st);
+                          double* rh, double* rl, double* ilh, double* ill, double* iuh, double* iul,
+                          int tcmode = 0) {
+    gb_status e = lu_run_core<M>(s, A, lda, W, perm, piv, st, tcmode);
     if (e != GB_OK) return e;
     count_launch(2);
     k_lu_rcp<S><<<std::max(1, std::min(1184, (s->n + 255) / 256)), 256, 0, s->stream>>>(W, s->lda, s->n, rh, rl);
@@ -982,11 +983,12 @@ struct Impl {
   }
 
   template <int M, class TA, class S>
-  static gb_status lu_run_core(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st) {
+  static gb_status lu_run_core(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st,
+                               int tcmode = 0) {
     const int n = s->n;
     LuStatus init{0x7fffffff, 0, 0ull, 0ull};
     CK(cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
-    if (n <= 128 && M == MODE_H16) {
+    if (n <= 128 && M == MODE_H16 && tcmode == 0) {
       size_t sm = (size_t)n * n * sizeof(typename LuT<M>::C);
       gb_status e = set_smem(k_lu_small<M, TA>, sm);
       if (e != GB_OK) return e;
@@ -1007,7 +1009,7 @@ struct Impl {
       auto kern = k_lu_team<M, TA, CtaTeam>;
       gb_status e = set_smem(kern, smb);
       if (e != GB_OK) return e;
-      kern<<<1, 256, smb, s->stream>>>(A, lda, W, (size_t)s->lda, n, perm, st, wk, s->ctl, s->partials);
+      kern<<<1, 256, smb, s->stream>>>(A, lda, W, (size_t)s->lda, n, perm, st, wk, s->ctl, s->partials, tcmode);
       CK(cudaGetLastError());
     } else {
       auto kern = k_lu_team<M, TA, GridTeam>;
@@ -1016,8 +1018,8 @@ struct Impl {
       size_t ldw = (size_t)s->lda;
       GridCtl* ctl = s->ctl;
       double* part = s->partials;
-      void* argv[] = {(void*)&A, (void*)&lda, (void*)&W, (void*)&ldw, (void*)&n, (void*)&perm, (void*)&st,
-                      (void*)&wk, (void*)&ctl, (void*)&part};
+      void* argv[] = {(void*)&A,  (void*)&lda, (void*)&W,   (void*)&ldw,  (void*)&n,     (void*)&perm,
+                      (void*)&st, (void*)&wk,  (void*)&ctl, (void*)&part, (void*)&tcmode};
       CK(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(256), argv, smb, s->stream));
     }
     (void)piv;
@@ -1027,7 +1029,7 @@ struct Impl {
   static gb_status factor(gb_solver* s, int* zero_col, double* growth) {
     CK(cudaEventRecord(s->ev0, s->stream));
     gb_status e = lu_run<UM>(s, (const TW*)s->A, (size_t)s->lda, (typename LuT<UM>::S*)s->LU, s->perm, s->piv, s->lust,
-                             s->rcph, s->rcpl, s->linvh, s->linvl, s->uinvh, s->uinvl);
+                             s->rcph, s->rcpl, s->linvh, s->linvl, s->uinvh, s->uinvl, s->o.lu_mode);
     if (e != GB_OK) return e;
     CK(cudaEventRecord(s->ev1, s->stream));
     LuStatus h;

@@ -92,6 +92,10 @@ class RefineConfig:
     collect_diagnostics: bool = False
     restart_residual: str = "recurrence"
     cycle_residual: str = "recurrence"
+    # extension (not in the reference): "exact" reproduces the reference's
+    # u_f arithmetic bit for bit; "tensor" runs the fp16 trailing update on
+    # tcgen05 tensor cores with fp32 accumulation (pivots agree up to ties)
+    lu_mode: str = "exact"
 
     def resolved_tau(self) -> float:
         return self.tau if self.tau is not None else _DEFAULT_TAU[self.precisions.u]
@@ -192,7 +196,9 @@ def make_options(cfg: RefineConfig, n: int, grid_ctas: int = 0) -> _lib.Options:
     o.reorthogonalize = int(bool(cfg.reorthogonalize))
     o.extra_precision = int(cfg.resolved_extra_precision())
     o.grid_ctas = grid_ctas
-    o.lu_mode = 0
+    if cfg.lu_mode not in ("exact", "tensor"):
+        raise ValueError(f"unknown lu_mode {cfg.lu_mode!r}")
+    o.lu_mode = 1 if cfg.lu_mode == "tensor" else 0
     return o
 
 

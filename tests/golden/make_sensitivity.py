@@ -49,10 +49,25 @@ def _lane_sum(prod: np.ndarray, dt) -> float:
     return float(acc[0])
 
 
+_MODE = {"order": "lanes"}
+
+
+def _ordered_sum(prod: np.ndarray, dt) -> float:
+    mode = _MODE["order"]
+    if mode == "reversed":
+        acc = dt(0)
+        for v in prod[::-1]:
+            acc = dt(acc + v)
+        return float(acc)
+    if mode == "wide":  # accumulate in fp64, round once
+        return float(dt(np.sum(prod.astype(np.float64))))
+    return _lane_sum(prod, dt)
+
+
 def vdot_lanes(x, y, fmt):
     if fmt in (O.SINGLE, O.DOUBLE, O.QUAD):
         dt = np.float32 if fmt == O.SINGLE else np.float64
-        return _lane_sum(np.asarray(x, dt) * np.asarray(y, dt), dt)
+        return _ordered_sum(np.asarray(x, dt) * np.asarray(y, dt), dt)
     return _orig["vdot"](x, y, fmt)
 
 
@@ -104,10 +119,13 @@ def _set(lanes: bool, lu: bool):
 
 def envelope(a, b, prec, method, m, k, tau, i_max):
     runs = {}
-    for name, (lanes, lu) in {"ref": (False, False), "lanes": (True, False), "lu": (False, True),
-                              "both": (True, True)}.items():
+    variants = {"ref": (False, False, "lanes"), "lanes": (True, False, "lanes"), "lu": (False, True, "lanes"),
+                "both": (True, True, "lanes"), "reversed": (True, False, "reversed"),
+                "wide": (True, False, "wide")}
+    for name, (lanes, lu, order) in variants.items():
         if lu and prec[0] == "half":
             continue
+        _MODE["order"] = order
         _set(lanes, lu)
         try:
             rep = O.solve(a, b, tuple(prec), method, m, k, tau, i_max)

@@ -131,3 +131,40 @@ def test_operator_and_residual(gpu, tag, uf, u):
     np.testing.assert_allclose(rq, k[f"{tag}_res_q"], rtol=0, atol=1e-30 + 2 ** -52 * np.max(np.abs(rq)))
     np.testing.assert_allclose(rd, k[f"{tag}_res_d"], rtol=0, atol=100 * 2 ** -53 * sc)
     s.close()
+
+
+def test_lu_tensor_core_mode(gpu):
+    """lu_mode="tensor": tcgen05 trailing update (fp32 accumulation, rounded to
+    fp16).  Pivots agree with the exact mode on a prefix (they part at
+    near-ties), the backward error is at least as small, and a
+    config-1 solve reaches the same verdict and level."""
+    rng = np.random.default_rng(3)
+    n = 1024
+    a = rng.standard_normal((n, n))
+    a16 = a.astype(np.float32).astype(np.float16).astype(np.float64)
+    res = {}
+    for mode in ("exact", "tensor"):
+        cfg = RefineConfig(PrecisionTriple(Format.HALF, Format.SINGLE, Format.DOUBLE), method=Method.GMRES_IR,
+                           m=40, lu_mode=mode)
+        s = _lib.Solver(n, make_options(cfg, n))
+        s.set_system(a, np.ones(n))
+        zero, _ = s.factorize()
+        assert zero == -1
+        lu, perm = s.factors()
+        x = rng.standard_normal(n)
+        L, U = np.tril(lu, -1) + np.eye(n), np.triu(lu)
+        res[mode] = (perm, np.max(np.abs(a16[perm] @ x - L @ (U @ x))) / (np.max(np.abs(a16)) * np.max(np.abs(x))))
+        s.close()
+    d = np.nonzero(res["exact"][0] != res["tensor"][0])[0]
+    assert d.size == 0 or d[0] >= 16
+    assert res["tensor"][1] <= 2.0 * res["exact"][1]
+    from paper_2201_09827_b200.refine import _refine
+
+    a1, b1 = __import__("paper_2201_09827_b200.problems", fromlist=["x"]).config_problem(
+        __import__("paper_2201_09827_b200.problems", fromlist=["x"]).CONFIGS["cfg1"])
+    cfg = RefineConfig(PrecisionTriple(Format.HALF, Format.SINGLE, Format.DOUBLE), method=Method.RGMRES_IR, m=100,
+                       k=5, tau=1e-4, i_max=10, lu_mode="tensor")
+    rep = _refine(a1, b1, cfg)
+    g = golden_json("cfg1")["rgmres-ir"]
+    assert rep.converged and len(rep.inner_iters) == len(g["inner_iters"])
+    assert all(abs(x - y) <= 2 for x, y in zip(rep.inner_iters, g["inner_iters"]))
