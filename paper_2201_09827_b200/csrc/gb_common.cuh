@@ -23,6 +23,10 @@
 
 namespace gb {
 
+// per-32-row-block record of the TRSV helpers: the dd inverse of the diagonal
+// block (1024 doubles) followed by the folded neighbour block (1024 doubles)
+constexpr int kInvStride = 2048;
+
 // optional phase timers (globaltimer ns, CTA 0 thread 0); enabled per launch
 // by a non-null pointer.  slot 0 = count, then pairs (tag, t).
 struct PhaseLog {
@@ -125,9 +129,9 @@ GB_DEVICE dd warp_sum_dd(dd v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     dd w{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
-    // make the pairing order-symmetric so every lane ends with the same bits
-    int lane = threadIdx.x & 31;
-    v = (lane & o) ? dd_add(w, v) : dd_add(v, w);
+    // dd_add is commutative bit for bit (two_sum's error term is exact), so
+    // every lane ends with the same bits without a divergent pairing
+    v = dd_add(v, w);
   }
   return v;
 }

@@ -382,37 +382,44 @@ static __device__ __noinline__ double blk_cond2(double* b, int ld, int p, double
   }
   __shared__ double s_res[2];
   const int len = 2 * p - 1;
-  if (threadIdx.x < 2) {
-    // bound on the spectrum
+  // multisection on the ordered bit patterns of positive doubles: warp 0
+  // finds sigma_max, warp 1 sigma_min; each round the 32 lanes evaluate 32
+  // interior points (5 bits per round instead of 1 for plain bisection)
+  if (threadIdx.x < 64) {
+    const int lane = threadIdx.x & 31, wsel = threadIdx.x >> 5;
     double bnd = 0.0;
     for (int t = 0; t < len; ++t) {
-      double l = t > 0 ? fabs(bd[t - 1]) : 0.0;
+      const double l = t > 0 ? fabs(bd[t - 1]) : 0.0;
       bnd = fmax(bnd, l + fabs(bd[t]));
     }
     bnd = fmax(bnd, fabs(bd[len - 1]));
     bnd = bnd * (1.0 + 4.0 * kEps52) + 1e-300;
-    // bisection on the ordered bit patterns of positive doubles
-    const double target = threadIdx.x == 0 ? (double)(2 * p) : (double)(p + 1);
+    const double target = wsel == 0 ? (double)(2 * p) : (double)(p + 1);
     unsigned long long lo = 0ull, hi = (unsigned long long)__double_as_longlong(bnd);
-    if (threadIdx.x == 0) {
-      // largest: smallest x with count(x) >= 2p
-      while (hi - lo > 1) {
-        unsigned long long mid = lo + (hi - lo) / 2;
-        if (tgk_count(bd, len, __longlong_as_double((long long)mid)) >= target) hi = mid;
-        else lo = mid;
-      }
+    bool singular = false;
+    if (wsel == 1) singular = tgk_count(bd, len, __longlong_as_double(1ll)) >= target;
+    if (singular) {
+      hi = 0ull;
     } else {
-      if (tgk_count(bd, len, __longlong_as_double(1ll)) >= target) {
-        hi = 0ull;  // exactly singular
-      } else {
-        while (hi - lo > 1) {
-          unsigned long long mid = lo + (hi - lo) / 2;
-          if (tgk_count(bd, len, __longlong_as_double((long long)mid)) >= target) hi = mid;
-          else lo = mid;
+      while (hi - lo > 1) {
+        const unsigned long long span = hi - lo;
+        const unsigned long long step = span / 33 > 0 ? span / 33 : 1;
+        unsigned long long mid = lo + step * (unsigned long long)(lane + 1);
+        if (mid >= hi) mid = hi - 1;
+        const bool ok = tgk_count(bd, len, __longlong_as_double((long long)mid)) >= target;
+        const unsigned mask = __ballot_sync(0xffffffffu, ok);
+        if (mask == 0u) {
+          lo = __shfl_sync(0xffffffffu, mid, 31);
+        } else {
+          const int f = __ffs(mask) - 1;
+          const unsigned long long mf = __shfl_sync(0xffffffffu, mid, f);
+          const unsigned long long mp = f > 0 ? __shfl_sync(0xffffffffu, mid, f - 1) : lo;
+          hi = mf;
+          lo = f > 0 ? mp : lo;
         }
       }
     }
-    s_res[threadIdx.x] = __longlong_as_double((long long)hi);
+    if (lane == 0) s_res[wsel] = __longlong_as_double((long long)hi);
   }
   __syncthreads();
   double smax = s_res[0], smin = s_res[1];
@@ -646,9 +653,10 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           r = notlast ? H[IX(k + 2, k - 1, ld)] : 0.0;
           x = fabs(p_) + fabs(q) + fabs(r);
           if (x == 0.0) continue;
-          p_ = p_ / x;
-          q = q / x;
-          r = r / x;
+          const double rx = 1.0 / x;  // one division instead of three
+          p_ = p_ * rx;
+          q = q * rx;
+          r = r * rx;
         }
         s = sqrt(p_ * p_ + q * q + r * r);
         if (p_ < 0) s = -s;
@@ -660,11 +668,12 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           }
           __syncwarp();
           p_ = p_ + s;
-          x = p_ / s;
-          y = q / s;
-          z = r / s;
-          q = q / p_;
-          r = r / p_;
+          const double rs = 1.0 / s, rp = 1.0 / p_;
+          x = p_ * rs;
+          y = q * rs;
+          z = r * rs;
+          q = q * rp;
+          r = r * rp;
           for (int j = k + lane; j < nn; j += 32) {
             double pp = H[IX(k, j, ld)] + q * H[IX(k + 1, j, ld)];
             if (notlast) {

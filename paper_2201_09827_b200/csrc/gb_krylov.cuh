@@ -48,7 +48,14 @@ struct Krylov {
   int* cycle_keff;   // [max_cycles + 1]
   // recycle state carried across solves
   int* keff_io;  // [1]
+  // leader fast scratch in shared memory (reuses the TRSV tile region while
+  // no substitution is running); nullptr -> global scratch only
+  double* fast;
+  int fast_cap;  // doubles
 };
+
+// shared-memory need (doubles) of the leader's dense work at dimension p
+__host__ __device__ inline int leader_fast_need(int p, int kk) { return 3 * p * p + 5 * p * (kk + 2) + 8 * p + 64; }
 
 struct StepScalars {
   int ncycles, status, applies, keff;
@@ -725,7 +732,7 @@ __device__ void team_gram(Team& t, Krylov<TW, TA, TF, MV>& K, int keff, int j, d
 // with P, Q, R written to bc, or -1 (keep the previous space).
 // --------------------------------------------------------------------------
 template <class TW, class TA, class TF, int MV, class Team>
-__device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff, int j) {
+__device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff, int j, const PhaseLog& lg) {
   const int S = bc_S(K), kk = K.k;
   const int gr = keff + j + 1, gc = keff + j;
   double* Gm = K.dense;
@@ -765,9 +772,15 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
   }
   __syncthreads();
   if (s_flag) return -1;  // NoConvergence / SingularB propagate -> keep space
-  for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) b1c[e] = b1[e];
+  // shared-memory staging when it fits (the eigen iteration and the
+  // bidiagonalisation are latency bound: every scalar step touches the matrix)
+  const bool fast = K.fast != nullptr && leader_fast_need(gc, kk) <= K.fast_cap;
+  double* cmat = fast ? K.fast : b1c;
+  for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) cmat[e] = b1[e];
   __syncthreads();
-  double cnd = blk_cond2(b1c, gc, gc, bd, scr);
+  mark(lg, 60);
+  double cnd = blk_cond2(cmat, gc, gc, bd, scr);
+  mark(lg, 61);
   if (!(cnd <= 1.0 / kEps53)) {
     // shift by sqrt(u) * ||b1||_F and retry once (gcrodr.py:192-196)
     double f = 0.0;
@@ -777,17 +790,28 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
     const double shift = sqrt(kEps53) * sqrt(ff[0]);
     for (int e = threadIdx.x; e < gc; e += blockDim.x) b1[IX(e, e, gc)] += shift;
     __syncthreads();
-    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) b1c[e] = b1[e];
+    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) cmat[e] = b1[e];
     __syncthreads();
-    cnd = blk_cond2(b1c, gc, gc, bd, scr);
+    cnd = blk_cond2(cmat, gc, gc, bd, scr);
     if (!(cnd <= 1.0 / kEps53)) return -1;
   }
   // reduced = b1^-1 a1
   for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) rd[e] = a1[e];
   __syncthreads();
   if (blk_getrf(b1, gc, gc, piv) >= 0) return -1;
+  mark(lg, 62);
   blk_getrs(b1, gc, gc, piv, rd, gc, gc);
-  const int kn = leader_ritz_basis(rd, gc, kk, P, gc, scr);
+  mark(lg, 63);
+  double* emat = rd;
+  double* escr = scr;
+  if (fast) {
+    emat = K.fast;
+    escr = K.fast + (size_t)gc * gc;
+    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) emat[e] = rd[e];
+    __syncthreads();
+  }
+  const int kn = leader_ritz_basis(emat, gc, kk, P, gc, escr);
+  mark(lg, 64);
   if (kn <= 0) return -1;
   for (int e = threadIdx.x; e < gr * kn; e += blockDim.x) {
     int a = e % gr, b = e / gr;
@@ -797,6 +821,7 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
   }
   __syncthreads();
   if (!blk_qr_signed(GP, gr, gr, kn, Qs, gr, Rs, kk + 1, tau)) return -1;
+  mark(lg, 65);
   double* bP = bc_P(K);
   double* bQ = bc_Q(K);
   double* bR = bc_R(K);
@@ -894,7 +919,9 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
     }
     if (!K.recycling || !have_space) {
       // ---- plain GMRES(m) cycle (+ harvest for GCRO-DR) ----
+      mark(ts.log, 40);
       CycleOut co = arnoldi_cycle(t, K, ts, K.res, beta, M, tol, 0, true, sm, smem_ops, applies);
+      mark(ts.log, 41);
       const int j = co.steps;
       if (threadIdx.x == 0 && t.leader() && cycles <= K.max_cycles) {
         K.cycle_iters[cycles] = j;
@@ -953,7 +980,14 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
               __syncthreads();
             }
           }
-          int kn = leader_ritz_basis(Hm, j, kk, P, j, scr);
+          int kn;
+          if (K.fast != nullptr && leader_fast_need(j, kk) <= K.fast_cap) {
+            for (int e = threadIdx.x; e < j * j; e += blockDim.x) K.fast[e] = Hm[e];
+            __syncthreads();
+            kn = leader_ritz_basis(K.fast, j, kk, P, j, K.fast + (size_t)j * j);
+          } else {
+            kn = leader_ritz_basis(Hm, j, kk, P, j, scr);
+          }
           int status = -1;
           if (kn > 0) {
             // Hbar P  ((j+1) x kn)
@@ -1002,7 +1036,9 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
     }
     // ---- deflated cycle (gcrodr.py:342-390) ----
     const int budget = M - keff;
+    mark(ts.log, 50);
     CycleOut co = arnoldi_cycle(t, K, ts, K.res, beta, budget, tol, keff, false, sm, smem_ops, applies);
+    mark(ts.log, 51);
     const int j = co.steps;
     if (threadIdx.x == 0 && t.leader() && cycles <= K.max_cycles) K.cycle_iters[cycles] = j;
     cycles++;
@@ -1067,11 +1103,13 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
       }
       K.res[r] = rr;
     }
+    mark(ts.log, 52);
     if (j >= 1) {
       // W^T Vh (gr x gc) in the work format: per-CTA partial Grams
       team_gram(t, K, keff, j, sm);
+      mark(ts.log, 53);
       if (t.leader()) {
-        int kn = leader_recycle(t, K, keff, j);
+        int kn = leader_recycle(t, K, keff, j, ts.log);
         if (threadIdx.x == 0) K.bc[M + kk + 1] = (double)kn;
         __syncthreads();
       }
@@ -1087,6 +1125,7 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
       }
     }
     if (threadIdx.x == 0 && t.leader() && cycles - 1 <= K.max_cycles) K.cycle_keff[cycles - 1] = keff;
+    mark(ts.log, 55);
     first = false;
   }
   t.sync();

@@ -397,8 +397,8 @@ __device__ void diag_inv_block(const S* W, size_t ld, int n, int b, double* lh, 
     }
   }
   for (int i = 0; i < 32; ++i) {
-    lh[(size_t)b * 1024 + c * 32 + i] = (i > c && c < m) ? x[i].hi : 0.0;
-    ll[(size_t)b * 1024 + c * 32 + i] = (i > c && c < m) ? x[i].lo : 0.0;
+    lh[(size_t)b * kInvStride + c * 32 + i] = (i > c && c < m) ? x[i].hi : 0.0;
+    ll[(size_t)b * kInvStride + c * 32 + i] = (i > c && c < m) ? x[i].lo : 0.0;
     x[i] = dd{0.0, 0.0};
   }
   if (c < m) {
@@ -411,9 +411,61 @@ __device__ void diag_inv_block(const S* W, size_t ld, int n, int b, double* lh, 
     }
   }
   for (int i = 0; i < 32; ++i) {
-    uh[(size_t)b * 1024 + c * 32 + i] = (i <= c && c < m) ? x[i].hi : 0.0;
-    ul[(size_t)b * 1024 + c * 32 + i] = (i <= c && c < m) ? x[i].lo : 0.0;
+    uh[(size_t)b * kInvStride + c * 32 + i] = (i <= c && c < m) ? x[i].hi : 0.0;
+    ul[(size_t)b * kInvStride + c * 32 + i] = (i <= c && c < m) ? x[i].lo : 0.0;
   }
+}
+
+// Folded off-diagonal blocks for trsv_cta (second half of each block record,
+// row-major, element (i, j) at b*kInvStride + 1024 + i*32 + j):
+//   lower b >= 1:      D_b^-1 L_{b,b-1}   (D_b unit lower diagonal block)
+//   upper b <= nb - 2: U_bb^-1 U_{b,b+1}
+// so the block solve becomes y_b = D_b^-1 t' - M_b y_adjacent with t' free of
+// the adjacent block: only one 32-term product waits on the neighbour.
+template <class S>
+__device__ void diag_fold_block(const S* W, size_t ld, int n, int b, double* lh, double* ll, double* uh,
+                                double* ul) {
+  const int j = threadIdx.x & 31;
+  const int nb = (n + 31) / 32;
+  const int r0 = b * 32;
+  const int m = min(32, n - r0);
+  double* fl_h = lh + (size_t)b * kInvStride + 1024;
+  double* fl_l = ll + (size_t)b * kInvStride + 1024;
+  double* fu_h = uh + (size_t)b * kInvStride + 1024;
+  double* fu_l = ul + (size_t)b * kInvStride + 1024;
+  const double* Li_h = lh + (size_t)b * kInvStride;
+  const double* Li_l = ll + (size_t)b * kInvStride;
+  const double* Ui_h = uh + (size_t)b * kInvStride;
+  const double* Ui_l = ul + (size_t)b * kInvStride;
+  for (int i = 0; i < 32; ++i) {
+    dd sl{0.0, 0.0}, su{0.0, 0.0};
+    if (i < m) {
+      if (b >= 1) {
+        const int c = (b - 1) * 32 + j;
+        sl = dd{to_d(W[(size_t)(r0 + i) * ld + c]), 0.0};
+        for (int k = 0; k < i; ++k)
+          sl = dd_add(sl, dd_scale(to_d(W[(size_t)(r0 + k) * ld + c]), dd{Li_h[k * 32 + i], Li_l[k * 32 + i]}));
+      }
+      if (b + 1 < nb) {
+        const int c = (b + 1) * 32 + j;
+        if (c < n)
+          for (int k = i; k < m; ++k)
+            su = dd_add(su, dd_scale(to_d(W[(size_t)(r0 + k) * ld + c]), dd{Ui_h[k * 32 + i], Ui_l[k * 32 + i]}));
+      }
+    }
+    fl_h[i * 32 + j] = sl.hi;
+    fl_l[i * 32 + j] = sl.lo;
+    fu_h[i * 32 + j] = su.hi;
+    fu_l[i * 32 + j] = su.lo;
+  }
+}
+
+template <class S>
+__global__ void k_diag_fold(const S* W, size_t ld, int n, double* lh, double* ll, double* uh, double* ul) {
+  const int wpb = blockDim.x / 32;
+  const int nb = (n + 31) / 32;
+  for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < nb; b += gridDim.x * wpb)
+    diag_fold_block(W, ld, n, b, lh, ll, uh, ul);
 }
 
 template <class S>

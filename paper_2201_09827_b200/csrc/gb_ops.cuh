@@ -159,7 +159,8 @@ struct SysView {
   const double* rcp_lo;
   // dd-accurate inverses of the 32x32 diagonal blocks of L (strictly lower
   // part, unit diagonal implied) and U; element (i, j) of block b at
-  // b*1024 + j*32 + i.  nullptr -> sequential substitution.
+  // b*kInvStride + j*32 + i, followed by the folded off-diagonal block
+  // (diag_fold_block).  nullptr -> sequential substitution.
   const double* linv_hi;
   const double* linv_lo;
   const double* uinv_hi;
@@ -173,6 +174,7 @@ struct TrsvSync {
   unsigned long long epoch;  // call index; identical in all CTAs
   PhaseLog log;              // optional phase timers
   unsigned long long* stamps = nullptr;  // diagnostics: per block (deps seen, published)
+  uint4* ytag = nullptr;  // tagged copy of y for trsv_cta (2 x 16 B per entry)
 };
 
 GB_DEVICE unsigned long long ld_acquire64(const unsigned long long* p) {
@@ -240,7 +242,12 @@ GB_DEVICE void wait_ctr(unsigned long long* gctr, volatile unsigned long long* s
   if (cache >= target) return;
   unsigned long long v;
   if constexpr (Team::kGrid) {
-    while ((v = ld_relaxed64(gctr)) < target) __nanosleep(8);
+#ifndef GB_SPIN_NS
+#define GB_SPIN_NS 8
+#endif
+    while ((v = ld_relaxed64(gctr)) < target) {
+      if (GB_SPIN_NS > 0) __nanosleep(GB_SPIN_NS);
+    }
     fence_acq_rel();
   } else {
     while ((v = *sctr) < target) {
@@ -334,8 +341,8 @@ __device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename A
       if (inv_h != nullptr) {
         // y_b = inv(D_b) t_b as a 32-term dot per lane (no sequential chain);
         // lower: unit diagonal implied (strictly lower part stored)
-        const double* ih = inv_h + (size_t)b * 1024 + lane;
-        const double* il = inv_l != nullptr ? inv_l + (size_t)b * 1024 + lane : nullptr;
+        const double* ih = inv_h + (size_t)b * kInvStride + lane;
+        const double* il = inv_l != nullptr ? inv_l + (size_t)b * kInvStride + lane : nullptr;
         T s0 = kLower ? acc : Ar::zero(), s1 = Ar::zero(), s2 = Ar::zero(), s3 = Ar::zero();
 #pragma unroll
         for (int jj = 0; jj < 32; jj += 4) {
@@ -392,9 +399,300 @@ __device__ void trsv_blocks(Team& t, int n, const TF* LU, size_t ldf, typename A
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// super-block triangular solve for the non-exact modes (F64 / DD): a CTA owns
+// 256 rows (warp w: rows 32w..32w+31).  Off-diagonal super-blocks are consumed
+// as the grid-wide progress counter publishes them (8 tiles per warp, ILP
+// sums); the diagonal super-block is an in-CTA warp chain through shared
+// memory (diagonal 32x32 blocks applied through their dd inverses).  One
+// global hand-off per 256 rows instead of per 32 rows.
+// ---------------------------------------------------------------------------
+template <int M, class Team, class TF, bool kLower>
+__device__ void trsv_super(Team& t, int n, const TF* LU, size_t ldf, typename Arith<M>::T* y, const TrsvSync& ts,
+                           void* smem_raw, const double* inv_h, const double* inv_l) {
+  using Ar = Arith<M>;
+  using T = typename Ar::T;
+  using TT = typename TileT<TF>::T;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int SB = nw * 32;
+  const int nsb = (n + SB - 1) / SB;
+  TT* tile = reinterpret_cast<TT*>(smem_raw) + wid * 32 * 33;
+  T* ysb = reinterpret_cast<T*>(reinterpret_cast<TT*>(smem_raw) + nw * 32 * 33);  // SB entries
+  __shared__ volatile int s_cnt;  // sub-blocks of the current super-block finalised
+  unsigned long long* gctr = kLower ? ts.fwd : ts.bwd;
+  // same epoch base as trsv_blocks (32-row units) so the counters stay
+  // monotone when the two solvers alternate on one TrsvSync
+  const unsigned long long base = ts.epoch * (unsigned long long)((n + 31) / 32);
+  unsigned long long cache = 0;
+  if (!kLower && Team::kGrid) {
+    // the backward sweep starts from the bottom of the completed forward result
+    wait_ctr<Team>(ts.fwd, nullptr, base + (unsigned long long)nsb, cache);
+    cache = 0;
+  }
+  const int G = t.size(), r = t.rank();
+  for (int s = r; s < nsb; s += G) {
+    const int b = kLower ? s : nsb - 1 - s;
+    const int row0 = b * SB + wid * 32;
+    const int row = row0 + lane;
+    const bool rv = row < n;
+    T acc = rv ? Ar::ld(y + row) : Ar::zero();
+    if (threadIdx.x == 0) s_cnt = 0;
+    // off-diagonal super-blocks in sweep order, nw tiles each
+    const int noff = kLower ? b : nsb - 1 - b;
+    const int ntiles = noff * nw;
+    TT v[32];
+    auto tile_col = [&](int q) {
+      const int sbi = q / nw, tt = q % nw;
+      const int cb = kLower ? sbi : nsb - 1 - sbi;
+      return cb * SB + (kLower ? tt : nw - 1 - tt) * 32;
+    };
+    if (ntiles > 0 && row0 < n) tile_regs(v, LU, ldf, n, row0, tile_col(0));
+    for (int q = 0; q < ntiles; ++q) {
+      const int c0 = tile_col(q);
+      __syncwarp();
+      if (row0 < n) tile_store(tile, v);
+      if (q + 1 < ntiles && row0 < n) tile_regs(v, LU, ldf, n, row0, tile_col(q + 1));
+      if (q % nw == 0) wait_ctr<Team>(gctr, nullptr, base + (unsigned long long)(q / nw + 1), cache);
+      __syncwarp();
+      if (row0 >= n || c0 >= n) continue;
+      const T yv = (c0 + lane < n) ? Ar::ld(y + c0 + lane) : Ar::zero();
+      T s0 = Ar::zero(), s1 = Ar::zero(), s2 = Ar::zero(), s3 = Ar::zero();
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 4) {
+        s0 = Ar::mac_t(s0, (double)tile[lane * 33 + jj], Ar::shfl(yv, jj));
+        s1 = Ar::mac_t(s1, (double)tile[lane * 33 + jj + 1], Ar::shfl(yv, jj + 1));
+        s2 = Ar::mac_t(s2, (double)tile[lane * 33 + jj + 2], Ar::shfl(yv, jj + 2));
+        s3 = Ar::mac_t(s3, (double)tile[lane * 33 + jj + 3], Ar::shfl(yv, jj + 3));
+      }
+      acc = Ar::sub(acc, Ar::add(Ar::add(s0, s1), Ar::add(s2, s3)));
+    }
+    __syncthreads();
+    // diagonal super-block: in-CTA chain over the sub-blocks
+    const int nvalid = min(nw, (n - b * SB + 31) / 32);  // sub-blocks with rows < n
+    for (int st = 0; st < nvalid; ++st) {
+      const int w = kLower ? st : nvalid - 1 - st;  // sub-block finalised at this step
+      const int d0 = b * SB + w * 32;
+      if (row0 >= n) continue;
+      if (wid == w) {
+        // y_w = inv(D_w) t_w  (lower: unit diagonal implied)
+        const double* ih = inv_h + (size_t)(b * nw + w) * kInvStride + lane;
+        const double* il = inv_l != nullptr ? inv_l + (size_t)(b * nw + w) * kInvStride + lane : nullptr;
+        T q0 = kLower ? acc : Ar::zero(), q1 = Ar::zero(), q2 = Ar::zero(), q3 = Ar::zero();
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          q0 = Ar::mac_inv(q0, __ldg(ih + jj * 32), il ? __ldg(il + jj * 32) : 0.0, Ar::shfl(acc, jj));
+          q1 = Ar::mac_inv(q1, __ldg(ih + (jj + 1) * 32), il ? __ldg(il + (jj + 1) * 32) : 0.0,
+                           Ar::shfl(acc, jj + 1));
+          q2 = Ar::mac_inv(q2, __ldg(ih + (jj + 2) * 32), il ? __ldg(il + (jj + 2) * 32) : 0.0,
+                           Ar::shfl(acc, jj + 2));
+          q3 = Ar::mac_inv(q3, __ldg(ih + (jj + 3) * 32), il ? __ldg(il + (jj + 3) * 32) : 0.0,
+                           Ar::shfl(acc, jj + 3));
+        }
+        acc = Ar::add(Ar::add(q0, q1), Ar::add(q2, q3));
+        ysb[w * 32 + lane] = acc;
+        if (rv) y[row] = acc;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) s_cnt = st + 1;
+      } else if (kLower ? (wid > w) : (wid < w)) {
+        // tile (wid, w) is independent of y_w: load it before waiting
+        tile_regs(v, LU, ldf, n, row0, d0);
+        tile_store(tile, v);
+        while (s_cnt < st + 1) {
+        }
+        __threadfence_block();
+        __syncwarp();
+        const T yv = ysb[w * 32 + lane];
+        T s0 = Ar::zero(), s1 = Ar::zero(), s2 = Ar::zero(), s3 = Ar::zero();
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          s0 = Ar::mac_t(s0, (double)tile[lane * 33 + jj], Ar::shfl(yv, jj));
+          s1 = Ar::mac_t(s1, (double)tile[lane * 33 + jj + 1], Ar::shfl(yv, jj + 1));
+          s2 = Ar::mac_t(s2, (double)tile[lane * 33 + jj + 2], Ar::shfl(yv, jj + 2));
+          s3 = Ar::mac_t(s3, (double)tile[lane * 33 + jj + 3], Ar::shfl(yv, jj + 3));
+        }
+        acc = Ar::sub(acc, Ar::add(Ar::add(s0, s1), Ar::add(s2, s3)));
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if constexpr (Team::kGrid) {
+      if (threadIdx.x < 32) {
+        __threadfence();
+        if (threadIdx.x == 0) st_release64(gctr, base + (unsigned long long)(s + 1));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-per-block triangular solve for the non-exact modes (F64 / DD) on a grid
+// team: 32-row block b is owned by one CTA; warp w holds rows 4w..4w+3 of the
+// block, lane = column inside a 32-column tile.  Products accumulate per
+// thread over all off-diagonal tiles (no per-tile reduction), so only the
+// last tile, one butterfly sum and the 32x32 inverse apply sit on the
+// dependency chain between blocks.  A dd tile owned by one lane per row costs
+// ~3.4k cycles of dependent dd arithmetic on sm_100a; here a link is one MAC
+// plus two 5-level butterflies.
+// ---------------------------------------------------------------------------
+template <int M>
+GB_DEVICE typename Arith<M>::T ar_warp_sum(typename Arith<M>::T v) {
+  if constexpr (M == MODE_DD) {
+    return warp_sum_dd(v);
+  } else {
+    return warp_sum(v);
+  }
+}
+
+// Tagged y entries: every 8-byte word carries 32 payload bits and a 32-bit
+// tag (sweep id), so a consumer that sees the tag in both words of an entry
+// has its value -- no progress counter, no fence, one L2 round trip.
+GB_DEVICE void ytag_put1(uint4* p, double v, unsigned tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
+               "r"((unsigned)(b >> 32)), "r"(tag)
+               : "memory");
+}
+GB_DEVICE bool ytag_get1(const uint4* p, unsigned tag, double& v) {
+  unsigned x, y, z, w;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+               : "l"(p)
+               : "memory");
+  v = __longlong_as_double((long long)(((unsigned long long)z << 32) | x));
+  return y == tag && w == tag;
+}
+GB_DEVICE void ytag_put(uint4* yt, int i, double v, unsigned tag) { ytag_put1(yt + 2 * i, v, tag); }
+GB_DEVICE void ytag_put(uint4* yt, int i, dd v, unsigned tag) {
+  ytag_put1(yt + 2 * i, v.hi, tag);
+  ytag_put1(yt + 2 * i + 1, v.lo, tag);
+}
+GB_DEVICE bool ytag_get(const uint4* yt, int i, unsigned tag, double& v) { return ytag_get1(yt + 2 * i, tag, v); }
+GB_DEVICE bool ytag_get(const uint4* yt, int i, unsigned tag, dd& v) {
+  const bool a = ytag_get1(yt + 2 * i, tag, v.hi);
+  const bool b = ytag_get1(yt + 2 * i + 1, tag, v.lo);
+  return a && b;
+}
+// warp-uniform poll: every lane waits for its own entry (invalid lanes: zero)
+template <int M>
+GB_DEVICE typename Arith<M>::T ytag_wait(const uint4* yt, int i, bool valid, unsigned tag) {
+  typename Arith<M>::T v = Arith<M>::zero();
+  bool ok = !valid || ytag_get(yt, i, tag, v);
+  while (!__all_sync(0xffffffffu, ok)) {
+    if (!ok) ok = ytag_get(yt, i, tag, v);
+  }
+  return valid ? v : Arith<M>::zero();
+}
+
+template <int M, class Team, class TF, bool kLower>
+__device__ void trsv_cta(Team& t, int n, const TF* __restrict__ LU, size_t ldf, typename Arith<M>::T* y,
+                         const TrsvSync& ts, void* smem_raw, const double* __restrict__ inv_h,
+                         const double* __restrict__ inv_l) {
+  using Ar = Arith<M>;
+  using T = typename Ar::T;
+  constexpr int RPW = 4;  // rows per warp (8 warps x 4 = 32 rows)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nb = (n + 31) / 32;
+  T* tsh = reinterpret_cast<T*>(smem_raw);  // [2][32]: the block's reduced right-hand side
+  uint4* yt = ts.ytag;
+  const unsigned tag = (unsigned)(2ull * ts.epoch + (kLower ? 1ull : 2ull));
+  const unsigned ftag = (unsigned)(2ull * ts.epoch + 1ull);
+  const int G = t.size();
+  int it = 0;
+  for (int s = t.rank(); s < nb; s += G, ++it) {
+    const int b = kLower ? s : nb - 1 - s;
+    const int r0 = b * 32 + wid * RPW;  // first of this warp's rows
+    const int noff = kLower ? b : nb - 1 - b;
+    const int nfar = noff > 0 ? noff - 1 : 0;  // tiles before the adjacent block
+    // block inverse (column-major) and folded neighbour block (row-major)
+    double ih[RPW], il[RPW], mh[RPW], ml[RPW];
+    const double* rec_h = inv_h + (size_t)b * kInvStride;
+    const double* rec_l = inv_l + (size_t)b * kInvStride;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int ri = wid * RPW + i;
+      ih[i] = __ldg(rec_h + lane * 32 + ri);
+      il[i] = __ldg(rec_l + lane * 32 + ri);
+      mh[i] = __ldg(rec_h + 1024 + ri * 32 + lane);
+      ml[i] = __ldg(rec_l + 1024 + ri * 32 + lane);
+    }
+    // own rows' input: lower -> permuted right-hand side; upper -> forward result
+    T y0[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = r0 + i;
+      if (kLower)
+        y0[i] = r < n ? Ar::ld(y + r) : Ar::zero();
+      else
+        y0[i] = ytag_wait<M>(yt, r, r < n, ftag);
+    }
+    T acc[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) acc[i] = Ar::zero();
+    double lv[RPW], ln[RPW];
+    auto load_tile = [&](double (&d)[RPW], int q) {
+      const int c = (kLower ? q : nb - 1 - q) * 32 + lane;
+#pragma unroll
+      for (int i = 0; i < RPW; ++i)
+        d[i] = (r0 + i < n && c < n) ? to_d(LU[(size_t)(r0 + i) * ldf + c]) : 0.0;
+    };
+    if (nfar > 0) load_tile(lv, 0);
+    for (int q = 0; q < nfar; ++q) {
+      if (q + 1 < nfar) load_tile(ln, q + 1);
+      const int c = (kLower ? q : nb - 1 - q) * 32 + lane;
+      const T yc = ytag_wait<M>(yt, c, c < n, tag);
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) acc[i] = Ar::mac_t(acc[i], lv[i], yc);
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) lv[i] = ln[i];
+    }
+    // t' = y0 - (far tiles), reduced across the lanes (every lane gets it)
+    T tp[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      if (nfar > 0) acc[i] = ar_warp_sum<M>(acc[i]);
+      tp[i] = Ar::sub(y0[i], acc[i]);
+    }
+    T* tb = tsh + (it & 1) * 32;
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) tb[wid * RPW + i] = tp[i];
+    }
+    __syncthreads();
+    // z = D_b^-1 t'  (lower: unit diagonal implied)
+    const T tj = tb[lane];
+    T z[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      z[i] = ar_warp_sum<M>(Ar::mac_inv(Ar::zero(), ih[i], il[i], tj));
+      if (kLower) z[i] = Ar::add(z[i], tp[i]);
+    }
+    if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s] = gtimer();
+    // y_b = z - M_b y_adjacent
+    if (noff > 0) {
+      const int c = (kLower ? b - 1 : b + 1) * 32 + lane;
+      const T yc = ytag_wait<M>(yt, c, c < n, tag);
+      if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s + 2] = gtimer();
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) z[i] = Ar::sub(z[i], ar_warp_sum<M>(Ar::mac_inv(Ar::zero(), mh[i], ml[i], yc)));
+    }
+    T mine = z[0];
+#pragma unroll
+    for (int i = 1; i < RPW; ++i) mine = lane == i ? z[i] : mine;
+    if (lane < RPW && r0 + lane < n) {
+      ytag_put(yt, r0 + lane, mine, tag);
+      y[r0 + lane] = mine;
+    }
+    if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s + 1] = gtimer();
+  }
+}
+
 template <int M, class TF>
 __host__ __device__ inline size_t trsv_smem_bytes(int nthreads) {
-  return (size_t)(nthreads / 32) * 32 * 33 * sizeof(typename TileT<TF>::T);
+  return (size_t)(nthreads / 32) * 32 * 33 * sizeof(typename TileT<TF>::T) +
+         (size_t)nthreads * sizeof(typename Arith<M>::T);
 }
 
 // ---------------------------------------------------------------------------
@@ -504,9 +802,28 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
   t.sync();
   mark(ts.log, 11);
   // 2. forward (unit lower) then backward (upper)
-  trsv_blocks<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, nullptr, nullptr, s.linv_hi, s.linv_lo);
-  mark(ts.log, 12);
-  trsv_blocks<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.rcp_hi, s.rcp_lo, s.uinv_hi, s.uinv_lo);
+  bool done = false;
+  if constexpr (Team::kGrid && Arith<M>::kInv) {
+    if (s.linv_hi != nullptr && s.uinv_hi != nullptr && ts.ytag != nullptr) {
+      trsv_cta<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.linv_hi, s.linv_lo);
+      mark(ts.log, 12);
+      trsv_cta<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.uinv_hi, s.uinv_lo);
+      done = true;
+    }
+  }
+  if constexpr (!Team::kGrid && Arith<M>::kInv) {
+    if (s.linv_hi != nullptr && s.uinv_hi != nullptr) {
+      trsv_super<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.linv_hi, s.linv_lo);
+      mark(ts.log, 12);
+      trsv_super<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.uinv_hi, s.uinv_lo);
+      done = true;
+    }
+  }
+  if (!done) {
+    trsv_blocks<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, nullptr, nullptr, s.linv_hi, s.linv_lo);
+    mark(ts.log, 12);
+    trsv_blocks<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.rcp_hi, s.rcp_lo, s.uinv_hi, s.uinv_lo);
+  }
   mark(ts.log, 13);
   ts.epoch++;
   // 3. round to u (rows of this CTA's slice; the backward sweep is complete

@@ -76,6 +76,7 @@ struct Prob {
   int ur, method;
   unsigned long long* ctr;    // [2]
   unsigned long long* epoch;  // [1]
+  uint4* ytag = nullptr;      // tagged y of trsv_cta (2 x 16 B per entry)
   GridCtl* ctl;
   double* partials;
   int kmax;
@@ -125,6 +126,7 @@ __device__ void x0_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   constexpr int UM = UfMode<TF>::M;
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
+  ts.ytag = P.ytag;
   double* red = sm + 4 * K.m + 4;
   t.sync();
   op_apply<UM>(t, K.sys, (const TW*)nullptr, P.b, P.xs, reinterpret_cast<typename Arith<UM>::T*>(K.ybuf), ts,
@@ -153,6 +155,7 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   constexpr int UM = UfMode<TF>::M;
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch, P.log};
+  ts.ytag = P.ytag;
   mark(ts.log, 30);
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
@@ -212,6 +215,7 @@ template <class TW, class TF, int MV, class Team>
 __device__ void xref_refine_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
+  ts.ytag = P.ytag;
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
   SysView<TW, double> sx{n,       K.sys.lda, K.sys.A,  K.sys.lda, P.LUx,    P.permx,
@@ -245,6 +249,7 @@ template <int M, class TW, class TF, int MV, class Team>
 __device__ void debug_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops, int what) {
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
+  ts.ytag = P.ytag;
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
   int lo, hi;
@@ -286,6 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_step(Prob<TW, TF, MV> Pin) {
   Team t = MakeTeam<Team>::make(P);
   double* sm = reinterpret_cast<double*>(smem);
   void* ops = smem + sm_doubles(P.K.m, P.K.k) * sizeof(double);
+  P.K.fast = P.K.fast_cap > 0 ? reinterpret_cast<double*>(ops) : nullptr;
   step_body(t, P, sm, ops);
   if (t.leader() && threadIdx.x == 0) P.K.keff_io[1] = (P.K.U == Pin.K.U) ? 0 : 1;
 }
@@ -417,7 +423,7 @@ struct BatchArgs {
   int *converged, *steps, *reason, *inner, *flags;
   double *nbe, *ferr, *x, *growth;
   // options
-  int m, k, max_cycles, reorth, method, ur;
+  int m, k, max_cycles, reorth, method, ur, fast_cap;
   double tau;
 };
 
@@ -433,6 +439,7 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
   __shared__ double s_norm[2];
   char* base = B.slots + (size_t)blockIdx.x * B.L.stride;
   const SlotLayout& Ly = B.L;
+  const int fcap = B.fast_cap;
   const int n = B.n, ldv = (n + 31) & ~31;
   Prob<TW, TF, MV> P;
   memset(&P, 0, sizeof(P));
@@ -483,6 +490,8 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
   K.cycle_iters = (int*)(base + Ly.cyc_it);
   K.cycle_keff = (int*)(base + Ly.cyc_ke);
   K.keff_io = (int*)(base + Ly.keff_io);
+  K.fast = fcap > 0 ? reinterpret_cast<double*>(ops) : nullptr;
+  K.fast_cap = fcap;
   P.b = (const TW*)(base + Ly.b);
   P.xs = (TW*)(base + Ly.xs);
   P.r = (double*)(base + Ly.r);
@@ -707,6 +716,7 @@ struct gb_solver {
   size_t gram_stride = 0;
   void* ybuf = nullptr;
   unsigned long long *ctr = nullptr, *epoch = nullptr, *norms = nullptr;
+  uint4* ytag = nullptr;
   unsigned long long* plog = nullptr;  // phase log (diagnostics), 1 + 2 * cap
   int plog_cap = 0;
   GridCtl* ctl = nullptr;
@@ -795,6 +805,8 @@ struct Impl {
     K.cycle_iters = s->cycle_iters;
     K.cycle_keff = s->cycle_keff;
     K.keff_io = s->keff_io;
+    K.fast = nullptr;
+    K.fast_cap = fast_cap(s->o.m, s->o.k);
     P.b = (const TW*)s->b;
     P.xs = (TW*)s->xs;
     P.r = s->r;
@@ -808,6 +820,7 @@ struct Impl {
                                                                               : METH_GCRODR;
     P.ctr = s->ctr;
     P.epoch = s->epoch;
+    P.ytag = s->ytag;
     P.ctl = s->ctl;
     P.partials = s->partials;
     P.kmax = s->kmax;
@@ -827,9 +840,17 @@ struct Impl {
     return P;
   }
 
-  static size_t smem_bytes(gb_solver* s) {
-    return sm_doubles(s->o.m, s->o.k) * sizeof(double) + ops_bytes<TW, TF, MV>();
+  // dynamic smem: the sm region + max(TRSV tiles, leader fast scratch when it fits)
+  static int fast_cap(int m, int k) {
+    const size_t need = (size_t)leader_fast_need(m + k + 2, k) * sizeof(double);
+    const size_t base = sm_doubles(m, k) * sizeof(double);
+    return (base + std::max(need, ops_bytes<TW, TF, MV>()) <= 200 * 1024) ? (int)(need / sizeof(double)) : 0;
   }
+  static size_t smem_bytes_for(int m, int k) {
+    const int fc = fast_cap(m, k);
+    return sm_doubles(m, k) * sizeof(double) + std::max(ops_bytes<TW, TF, MV>(), (size_t)fc * sizeof(double));
+  }
+  static size_t smem_bytes(gb_solver* s) { return smem_bytes_for(s->o.m, s->o.k); }
 
   template <class KernT, class... Args>
   static gb_status launch(gb_solver* s, KernT kern, Args... args) {
@@ -862,7 +883,7 @@ struct Impl {
       s->perm = a.take<int>(ldv);
       s->piv = a.take<int>(64);
       s->lust = a.take<LuStatus>(1);
-      const size_t ninv = (size_t)((n + 31) / 32) * 1024;
+      const size_t ninv = (size_t)((n + 31) / 32) * kInvStride;
       s->linvh = a.take<double>(ninv);
       s->linvl = a.take<double>(ninv);
       s->uinvh = a.take<double>(ninv);
@@ -907,6 +928,7 @@ struct Impl {
       s->ybuf = a.take<double2>(ldv);
       s->ctr = a.take<unsigned long long>(4);
       s->epoch = a.take<unsigned long long>(2);
+      s->ytag = a.take<uint4>(2 * (size_t)ldv);
       s->norms = a.take<unsigned long long>(2);
       s->ctl = a.take<GridCtl>(1);
       s->partials = a.take<double>((size_t)2 * s->G * s->kmax);
@@ -978,6 +1000,8 @@ struct Impl {
     k_lu_rcp<S><<<std::max(1, std::min(1184, (s->n + 255) / 256)), 256, 0, s->stream>>>(W, s->lda, s->n, rh, rl);
     const int nbk = (s->n + 31) / 32;
     k_diag_inv<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
+    count_launch();
+    k_diag_fold<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
     CK(cudaGetLastError());
     return GB_OK;
   }
@@ -1172,10 +1196,10 @@ struct Impl {
     Ly.perm = take(sizeof(int) * ldv);
     Ly.rcph = take(sizeof(double) * ldv);
     Ly.rcpl = take(sizeof(double) * ldv);
-    Ly.linvh = take(sizeof(double) * (size_t)ldv * 32);
-    Ly.linvl = take(sizeof(double) * (size_t)ldv * 32);
-    Ly.uinvh = take(sizeof(double) * (size_t)ldv * 32);
-    Ly.uinvl = take(sizeof(double) * (size_t)ldv * 32);
+    Ly.linvh = take(sizeof(double) * (size_t)ldv * (kInvStride / 32));
+    Ly.linvl = take(sizeof(double) * (size_t)ldv * (kInvStride / 32));
+    Ly.uinvh = take(sizeof(double) * (size_t)ldv * (kInvStride / 32));
+    Ly.uinvl = take(sizeof(double) * (size_t)ldv * (kInvStride / 32));
     Ly.xs = take(sizeof(TW) * ldv);
     Ly.r = take(sizeof(double) * ldv);
     Ly.xref = take(sizeof(double) * ldv);
@@ -1217,7 +1241,7 @@ struct Impl {
     Ly.xperm = take(sizeof(int) * ldv);
     Ly.stride = (off + 255) & ~size_t(255);
 
-    const size_t sm = sm_doubles(m, k) * sizeof(double) + ops_bytes<TW, TF, MV>();
+    const size_t sm = smem_bytes_for(m, k);
     gb_status e = set_smem(k_batched<TW, TF, MV>, sm);
     if (e != GB_OK) return e;
     int dev = 0, sms = 148, per = 1;
@@ -1275,6 +1299,7 @@ struct Impl {
                                                                           : METH_GCRODR;
     A.ur = o->ur == GB_QUAD ? UR_DD : (o->ur == GB_DOUBLE ? UR_F64 : UR_F32);
     A.tau = o->tau;
+    A.fast_cap = fast_cap(m, k);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));

@@ -21,6 +21,22 @@ t1 = time.perf_counter()
 cfg = RefineConfig(PrecisionTriple.parse(*spec.precisions), Method.parse(args.method), m=spec.m,
                    k=spec.k if args.method.startswith("r") else 0, tau=spec.tau, i_max=args.imax or spec.i_max)
 trace = []
+if os.environ.get("PHASES"):
+    import collections
+    from paper_2201_09827_b200 import _lib
+    orig_step = _lib.Solver.step
+    def step(self):
+        self.phaselog(200000, read=False)
+        info = orig_step(self)
+        log = self.phaselog(0)
+        acc = collections.defaultdict(float); cnt = collections.Counter()
+        for (t0, a0), (t1, b1) in zip(log[:-1], log[1:]):
+            acc[(t0, t1)] += (b1 - a0) / 1e3; cnt[(t0, t1)] += 1
+        tot = sum(acc.values())
+        for key, v in sorted(acc.items(), key=lambda kv: -kv[1])[:16]:
+            print("   %s->%s: %5.1f%% total %.1f us, n %d, avg %.2f us" % (key[0], key[1], 100 * v / tot, v, cnt[key], v / cnt[key]))
+        return info
+    _lib.Solver.step = step
 rep = _refine(a, b, cfg, trace=trace, grid_ctas=args.grid)
 t2 = time.perf_counter()
 print(f"gen {t1-t0:.1f}s solve {t2-t1:.2f}s")
