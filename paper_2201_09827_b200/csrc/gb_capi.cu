@@ -1,6 +1,8 @@
 // C ABI (include/gcrodr_b200.h): argument checks, dispatch over the
 // precision variants (each compiled in its own gb_var_*.cu) and the extern "C"
 // entry points.
+#include <cstdlib>
+#include <cstring>
 #include "gb_solver.cuh"
 
 const VariantOps* gb_variant_f_h_f64() __attribute__((weak));
@@ -82,6 +84,10 @@ gb_status gb_solver_create(gb_solver** out, int n, const gb_options* opt, void* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int want = o.grid_ctas > 0 ? o.grid_ctas : std::min(sms, std::max(2, (n + 63) / 64));
     s->G = std::min(want, sms);
+    // a team of <= 16 CTAs runs as one thread-block cluster (hardware
+    // barrier) unless GB_TEAM=grid asks for the cooperative grid barrier
+    const char* team = std::getenv("GB_TEAM");
+    s->cluster = s->G <= 16 && !(team && std::strcmp(team, "grid") == 0);
   }
   if (cudaEventCreate(&s->ev0) != cudaSuccess || cudaEventCreate(&s->ev1) != cudaSuccess) {
     delete s;

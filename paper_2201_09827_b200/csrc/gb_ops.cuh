@@ -175,6 +175,7 @@ struct TrsvSync {
   PhaseLog log;              // optional phase timers
   unsigned long long* stamps = nullptr;  // diagnostics: per block (deps seen, published)
   uint4* ytag = nullptr;  // tagged copy of y for trsv_cta (2 x 16 B per entry)
+  int dsm = 0;            // > 0: ytag is this CTA's shared-memory copy in a cluster of dsm CTAs
 };
 
 GB_DEVICE unsigned long long ld_acquire64(const unsigned long long* p) {
@@ -548,52 +549,204 @@ GB_DEVICE typename Arith<M>::T ar_warp_sum(typename Arith<M>::T v) {
 
 // Tagged y entries: every 8-byte word carries 32 payload bits and a 32-bit
 // tag (sweep id), so a consumer that sees the tag in both words of an entry
-// has its value -- no progress counter, no fence, one L2 round trip.
-GB_DEVICE void ytag_put1(uint4* p, double v, unsigned tag) {
+// has its value -- no progress counter, no fence, one round trip.
+//   dsm == 0: the tagged copy lives in global memory (L2 round trip per poll);
+//   dsm == G: the team is one thread-block cluster and every CTA holds its own
+//             copy in shared memory -- producers push each entry into all G
+//             copies (st.shared::cluster), consumers poll their local copy
+//             (measured on B200: polling a producer's copy over DSMEM instead
+//             is ~3x slower per link under contention).
+// (q0, qs): this thread pushes into cluster CTAs q0, q0 + qs, ... (the
+// producers of one entry split the G remote stores between them)
+GB_DEVICE void ytag_put1(uint4* p, double v, unsigned tag, int dsm, int q0 = 0, int qs = 1) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
-               "r"((unsigned)(b >> 32)), "r"(tag)
-               : "memory");
+  if (dsm == 0) {
+    if (q0 == 0)
+      asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
+                   "r"((unsigned)(b >> 32)), "r"(tag)
+                   : "memory");
+    return;
+  }
+  const unsigned la = (unsigned)__cvta_generic_to_shared(p);
+  for (int q = q0; q < dsm; q += qs) {
+    unsigned ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(q));
+    asm volatile("st.relaxed.cluster.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ra), "r"((unsigned)b),
+                 "r"(tag), "r"((unsigned)(b >> 32)), "r"(tag)
+                 : "memory");
+  }
 }
-GB_DEVICE bool ytag_get1(const uint4* p, unsigned tag, double& v) {
+GB_DEVICE bool ytag_get1(const uint4* p, unsigned tag, double& v, int dsm) {
   unsigned x, y, z, w;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-               : "l"(p)
-               : "memory");
+  if (dsm == 0) {
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                 : "l"(p)
+                 : "memory");
+  } else {
+    asm volatile("ld.relaxed.cluster.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p))
+                 : "memory");
+  }
   v = __longlong_as_double((long long)(((unsigned long long)z << 32) | x));
   return y == tag && w == tag;
 }
-GB_DEVICE void ytag_put(uint4* yt, int i, double v, unsigned tag) { ytag_put1(yt + 2 * i, v, tag); }
-GB_DEVICE void ytag_put(uint4* yt, int i, dd v, unsigned tag) {
-  ytag_put1(yt + 2 * i, v.hi, tag);
-  ytag_put1(yt + 2 * i + 1, v.lo, tag);
+GB_DEVICE void ytag_put(uint4* yt, int i, double v, unsigned tag, int dsm, int q0 = 0, int qs = 1) {
+  ytag_put1(yt + 2 * i, v, tag, dsm, q0, qs);
 }
-GB_DEVICE bool ytag_get(const uint4* yt, int i, unsigned tag, double& v) { return ytag_get1(yt + 2 * i, tag, v); }
-GB_DEVICE bool ytag_get(const uint4* yt, int i, unsigned tag, dd& v) {
-  const bool a = ytag_get1(yt + 2 * i, tag, v.hi);
-  const bool b = ytag_get1(yt + 2 * i + 1, tag, v.lo);
+GB_DEVICE void ytag_put(uint4* yt, int i, dd v, unsigned tag, int dsm, int q0 = 0, int qs = 1) {
+  ytag_put1(yt + 2 * i, v.hi, tag, dsm, q0, qs);
+  ytag_put1(yt + 2 * i + 1, v.lo, tag, dsm, q0, qs);
+}
+GB_DEVICE bool ytag_get(const uint4* yt, int i, unsigned tag, double& v, int dsm) {
+  return ytag_get1(yt + 2 * i, tag, v, dsm);
+}
+GB_DEVICE bool ytag_get(const uint4* yt, int i, unsigned tag, dd& v, int dsm) {
+  const bool a = ytag_get1(yt + 2 * i, tag, v.hi, dsm);
+  const bool b = ytag_get1(yt + 2 * i + 1, tag, v.lo, dsm);
   return a && b;
 }
 // warp-uniform poll: every lane waits for its own entry (invalid lanes: zero)
 template <int M>
-GB_DEVICE typename Arith<M>::T ytag_wait(const uint4* yt, int i, bool valid, unsigned tag) {
+GB_DEVICE typename Arith<M>::T ytag_wait(const uint4* yt, int i, bool valid, unsigned tag, int dsm) {
   typename Arith<M>::T v = Arith<M>::zero();
-  bool ok = !valid || ytag_get(yt, i, tag, v);
+  bool ok = !valid || ytag_get(yt, i, tag, v, dsm);
   while (!__all_sync(0xffffffffu, ok)) {
-    if (!ok) ok = ytag_get(yt, i, tag, v);
+    if (!ok) ok = ytag_get(yt, i, tag, v, dsm);
   }
   return valid ? v : Arith<M>::zero();
+}
+
+// Compensated accumulation of products (Ogita-Rump-Oishi Dot2 for the DD
+// mode): the exact product error and the two_sum error of every step are
+// summed in a running double, so the result carries the accuracy of
+// dd arithmetic (error <= u^2-level relative to sum |a_i y_i|) at ~10 fp64
+// operations per term instead of a full dd_add; F64: a plain fma chain.
+template <int M>
+struct CAcc;
+template <>
+struct CAcc<MODE_F64> {
+  double s = 0.0;
+  GB_DEVICE void add(double a, double y) { s = __fma_rn(a, y, s); }
+  // (ih, il) * t: the F64 mode keeps only the high part of dd records
+  GB_DEVICE void add_inv(double ih, double, double t) { s = __fma_rn(ih, t, s); }
+  GB_DEVICE void merge(const CAcc& o) { s = __dadd_rn(s, o.s); }
+  GB_DEVICE CAcc xor_shfl(int o) const {
+    CAcc r;
+    r.s = __shfl_xor_sync(0xffffffffu, s, o);
+    return r;
+  }
+  GB_DEVICE double get() const { return s; }
+};
+template <>
+struct CAcc<MODE_DD> {
+  double s = 0.0, c = 0.0;
+  GB_DEVICE void add(double a, double y) {
+    const double p = __dmul_rn(a, y);
+    const double e = __fma_rn(a, y, -p);
+    const double t = __dadd_rn(s, p);
+    const double v = __dsub_rn(t, s);
+    const double q = __dadd_rn(__dsub_rn(s, __dsub_rn(t, v)), __dsub_rn(p, v));
+    s = t;
+    c = __dadd_rn(c, __dadd_rn(q, e));
+  }
+  GB_DEVICE void add(double a, dd y) {
+    const double p = __dmul_rn(a, y.hi);
+    const double e = __fma_rn(a, y.lo, __fma_rn(a, y.hi, -p));
+    const double t = __dadd_rn(s, p);
+    const double v = __dsub_rn(t, s);
+    const double q = __dadd_rn(__dsub_rn(s, __dsub_rn(t, v)), __dsub_rn(p, v));
+    s = t;
+    c = __dadd_rn(c, __dadd_rn(q, e));
+  }
+  // (ih + il) * (t.hi + t.lo): exact leading product, first-order cross terms
+  GB_DEVICE void add_inv(double ih, double il, dd t) {
+    const double p = __dmul_rn(ih, t.hi);
+    const double e = __fma_rn(il, t.hi, __fma_rn(ih, t.lo, __fma_rn(ih, t.hi, -p)));
+    const double u = __dadd_rn(s, p);
+    const double v = __dsub_rn(u, s);
+    const double q = __dadd_rn(__dsub_rn(s, __dsub_rn(u, v)), __dsub_rn(p, v));
+    s = u;
+    c = __dadd_rn(c, __dadd_rn(q, e));
+  }
+  // symmetric in (this, o): every lane of a butterfly ends with the same bits
+  GB_DEVICE void merge(const CAcc& o) {
+    const double u = __dadd_rn(s, o.s);
+    const double v = __dsub_rn(u, s);
+    const double q = __dadd_rn(__dsub_rn(s, __dsub_rn(u, v)), __dsub_rn(o.s, v));
+    s = u;
+    c = __dadd_rn(__dadd_rn(c, o.c), q);
+  }
+  GB_DEVICE CAcc xor_shfl(int o) const {
+    CAcc r;
+    r.s = __shfl_xor_sync(0xffffffffu, s, o);
+    r.c = __shfl_xor_sync(0xffffffffu, c, o);
+    return r;
+  }
+  GB_DEVICE dd get() const { return fast_two_sum(s, c); }
+};
+
+template <int M>
+GB_DEVICE CAcc<M> cbfly8(CAcc<M> a) {
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) a.merge(a.xor_shfl(o));
+  return a;
+}
+
+// xor-butterfly over the 8 lanes of a row group (every lane ends with the same
+// bits: the per-mode add is commutative bit for bit)
+template <int M>
+GB_DEVICE typename Arith<M>::T bfly8(typename Arith<M>::T v) {
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    if constexpr (M == MODE_DD) {
+      dd w{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+      v = dd_add(v, w);
+    } else {
+      v = Arith<M>::add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+  }
+  return v;
+}
+
+// four consecutive factor entries of one row (zero past n), vectorised when
+// the run is in range (rows are padded to 32 entries, runs start at 4k)
+template <class TF>
+GB_DEVICE void load4(const TF* __restrict__ p, int c, int n, bool rowok, double (&d)[4]) {
+  if (rowok && c + 3 < n) {
+    if constexpr (sizeof(TF) == 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+      d[0] = v.x, d[1] = v.y, d[2] = v.z, d[3] = v.w;
+    } else if constexpr (sizeof(TF) == 2) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+      const __half2 a = *reinterpret_cast<const __half2*>(&v.x), b = *reinterpret_cast<const __half2*>(&v.y);
+      d[0] = __low2float(a), d[1] = __high2float(a), d[2] = __low2float(b), d[3] = __high2float(b);
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      d[0] = a.x, d[1] = a.y, d[2] = b.x, d[3] = b.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[j] = (rowok && c + j < n) ? to_d(p[j]) : 0.0;
+  }
 }
 
 template <int M, class Team, class TF, bool kLower>
 __device__ void trsv_cta(Team& t, int n, const TF* __restrict__ LU, size_t ldf, typename Arith<M>::T* y,
                          const TrsvSync& ts, void* smem_raw, const double* __restrict__ inv_h,
                          const double* __restrict__ inv_l) {
+  // Lane layout: warp w owns rows 4w..4w+3 of the 32-row block; inside the
+  // warp, lane = 8 * (row - 4w) + cg and lane cg covers the four columns
+  // 4cg..4cg+3 of every 32-column tile.  Every row sum is then four MACs per
+  // lane plus a 3-level butterfly over the row's 8 lanes, so the chain
+  // between blocks is 4 MACs + 3 shuffle levels (instead of one 5-level warp
+  // reduction per row).
   using Ar = Arith<M>;
   using T = typename Ar::T;
-  constexpr int RPW = 4;  // rows per warp (8 warps x 4 = 32 rows)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rq = lane >> 3, cg = lane & 7, c4 = cg * 4;
+  const int ri = wid * 4 + rq;  // row inside the block
   const int nb = (n + 31) / 32;
   T* tsh = reinterpret_cast<T*>(smem_raw);  // [2][32]: the block's reduced right-hand side
   uint4* yt = ts.ytag;
@@ -603,87 +756,75 @@ __device__ void trsv_cta(Team& t, int n, const TF* __restrict__ LU, size_t ldf, 
   int it = 0;
   for (int s = t.rank(); s < nb; s += G, ++it) {
     const int b = kLower ? s : nb - 1 - s;
-    const int r0 = b * 32 + wid * RPW;  // first of this warp's rows
+    const int r = b * 32 + ri;
+    const bool rowok = r < n;
     const int noff = kLower ? b : nb - 1 - b;
     const int nfar = noff > 0 ? noff - 1 : 0;  // tiles before the adjacent block
-    // block inverse (column-major) and folded neighbour block (row-major)
-    double ih[RPW], il[RPW], mh[RPW], ml[RPW];
+    // block inverse (column-major, [c * 32 + ri]) and folded neighbour block
+    // (row-major, [1024 + ri * 32 + c]) for this lane's four columns
+    double ih[4], il[4], mh[4], ml[4];
     const double* rec_h = inv_h + (size_t)b * kInvStride;
     const double* rec_l = inv_l + (size_t)b * kInvStride;
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int ri = wid * RPW + i;
-      ih[i] = __ldg(rec_h + lane * 32 + ri);
-      il[i] = __ldg(rec_l + lane * 32 + ri);
-      mh[i] = __ldg(rec_h + 1024 + ri * 32 + lane);
-      ml[i] = __ldg(rec_l + 1024 + ri * 32 + lane);
+    for (int j = 0; j < 4; ++j) {
+      ih[j] = __ldg(rec_h + (c4 + j) * 32 + ri);
+      il[j] = __ldg(rec_l + (c4 + j) * 32 + ri);
+      mh[j] = -__ldg(rec_h + 1024 + ri * 32 + c4 + j);
+      ml[j] = -__ldg(rec_l + 1024 + ri * 32 + c4 + j);
     }
-    // own rows' input: lower -> permuted right-hand side; upper -> forward result
-    T y0[RPW];
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int r = r0 + i;
-      if (kLower)
-        y0[i] = r < n ? Ar::ld(y + r) : Ar::zero();
-      else
-        y0[i] = ytag_wait<M>(yt, r, r < n, ftag);
-    }
-    T acc[RPW];
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) acc[i] = Ar::zero();
-    double lv[RPW], ln[RPW];
-    auto load_tile = [&](double (&d)[RPW], int q) {
-      const int c = (kLower ? q : nb - 1 - q) * 32 + lane;
-#pragma unroll
-      for (int i = 0; i < RPW; ++i)
-        d[i] = (r0 + i < n && c < n) ? to_d(LU[(size_t)(r0 + i) * ldf + c]) : 0.0;
-    };
-    if (nfar > 0) load_tile(lv, 0);
+    // own row's input: lower -> permuted right-hand side; upper -> forward result
+    T y0 = kLower ? (rowok ? Ar::ld(y + r) : Ar::zero()) : ytag_wait<M>(yt, r, rowok, ftag, ts.dsm);
+    CAcc<M> ca0, ca1;
+    double lv[4], ln[4];
+    const TF* lrow = LU + (size_t)(rowok ? r : 0) * ldf;
+    auto tile_col = [&](int q) { return (kLower ? q : nb - 1 - q) * 32; };
+    if (nfar > 0) load4<TF>(lrow + tile_col(0) + c4, tile_col(0) + c4, n, rowok, lv);
     for (int q = 0; q < nfar; ++q) {
-      if (q + 1 < nfar) load_tile(ln, q + 1);
-      const int c = (kLower ? q : nb - 1 - q) * 32 + lane;
-      const T yc = ytag_wait<M>(yt, c, c < n, tag);
+      const int tc = tile_col(q);
+      if (q + 1 < nfar) load4<TF>(lrow + tile_col(q + 1) + c4, tile_col(q + 1) + c4, n, rowok, ln);
+      const T yl = ytag_wait<M>(yt, tc + lane, tc + lane < n, tag, ts.dsm);
+      ca0.add(lv[0], Ar::shfl(yl, c4 + 0));
+      ca1.add(lv[1], Ar::shfl(yl, c4 + 1));
+      ca0.add(lv[2], Ar::shfl(yl, c4 + 2));
+      ca1.add(lv[3], Ar::shfl(yl, c4 + 3));
 #pragma unroll
-      for (int i = 0; i < RPW; ++i) acc[i] = Ar::mac_t(acc[i], lv[i], yc);
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) lv[i] = ln[i];
+      for (int j = 0; j < 4; ++j) lv[j] = ln[j];
     }
-    // t' = y0 - (far tiles), reduced across the lanes (every lane gets it)
-    T tp[RPW];
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      if (nfar > 0) acc[i] = ar_warp_sum<M>(acc[i]);
-      tp[i] = Ar::sub(y0[i], acc[i]);
+    // t' = y0 - (far tiles) for this row (all 8 lanes of the row hold it)
+    T acc = Ar::zero();
+    if (nfar > 0) {
+      ca0.merge(ca1);
+      acc = T(cbfly8<M>(ca0).get());
     }
+    const T tp = Ar::sub(y0, acc);
     T* tb = tsh + (it & 1) * 32;
-    if (lane == 0) {
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) tb[wid * RPW + i] = tp[i];
-    }
+    if (cg == 0) tb[ri] = tp;
     __syncthreads();
-    // z = D_b^-1 t'  (lower: unit diagonal implied)
-    const T tj = tb[lane];
-    T z[RPW];
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      z[i] = ar_warp_sum<M>(Ar::mac_inv(Ar::zero(), ih[i], il[i], tj));
-      if (kLower) z[i] = Ar::add(z[i], tp[i]);
-    }
+    // partial of D_b^-1 t' over this lane's columns (lower: unit diagonal
+    // implied), carried as a compensated pair through the chain below
+    CAcc<M> pa, pb;
+    pa.add_inv(ih[0], il[0], tb[c4 + 0]);
+    pb.add_inv(ih[1], il[1], tb[c4 + 1]);
+    pa.add_inv(ih[2], il[2], tb[c4 + 2]);
+    pb.add_inv(ih[3], il[3], tb[c4 + 3]);
     if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s] = gtimer();
-    // y_b = z - M_b y_adjacent
+    // y_b = D_b^-1 t' - M_b y_adjacent  (critical chain: 2 products deep,
+    // one pair merge, 3 butterfly merges)
     if (noff > 0) {
-      const int c = (kLower ? b - 1 : b + 1) * 32 + lane;
-      const T yc = ytag_wait<M>(yt, c, c < n, tag);
+      const int tc = (kLower ? b - 1 : b + 1) * 32;
+      const T yl = ytag_wait<M>(yt, tc + lane, tc + lane < n, tag, ts.dsm);
       if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s + 2] = gtimer();
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) z[i] = Ar::sub(z[i], ar_warp_sum<M>(Ar::mac_inv(Ar::zero(), mh[i], ml[i], yc)));
+      pa.add_inv(mh[0], ml[0], Ar::shfl(yl, c4 + 0));
+      pb.add_inv(mh[1], ml[1], Ar::shfl(yl, c4 + 1));
+      pa.add_inv(mh[2], ml[2], Ar::shfl(yl, c4 + 2));
+      pb.add_inv(mh[3], ml[3], Ar::shfl(yl, c4 + 3));
     }
-    T mine = z[0];
-#pragma unroll
-    for (int i = 1; i < RPW; ++i) mine = lane == i ? z[i] : mine;
-    if (lane < RPW && r0 + lane < n) {
-      ytag_put(yt, r0 + lane, mine, tag);
-      y[r0 + lane] = mine;
+    pa.merge(pb);
+    T z = T(cbfly8<M>(pa).get());
+    if (kLower) z = Ar::add(z, tp);
+    if (rowok) {
+      ytag_put(yt, r, z, tag, ts.dsm, cg, 8);  // the row's 8 lanes share the cluster pushes
+      if (cg == 0) y[r] = z;
     }
     if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s + 1] = gtimer();
   }
@@ -717,6 +858,51 @@ __device__ __forceinline__ typename Arith<M>::T row_dot_ex(const TA* __restrict_
   constexpr int VW = Vec16<TA>::N;
   constexpr int kU = 4;
   const int lane = threadIdx.x & 31;
+  if constexpr (M == MODE_DD) {
+    // compensated (Dot2) accumulation: exact products, two_sum errors summed
+    CAcc<MODE_DD> ca[kU];
+    double ab[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) ab[u] = 0.0;
+    const int nv = n / VW;
+    const Vec16<TA>* av = reinterpret_cast<const Vec16<TA>*>(arow);
+    int base = lane;
+    for (; base + 32 * (kU - 1) < nv; base += 32 * kU) {
+      Vec16<TA> a[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) a[u] = av[base + 32 * u];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          const double x = (double)a[u].v[e];
+          const double y = to_d(v[(base + 32 * u) * VW + e]);
+          ca[u].add(x, y);
+          if (kAbs) ab[u] = __fma_rn(fabs(x), fabs(y), ab[u]);
+        }
+      }
+    }
+    for (; base < nv; base += 32) {
+      Vec16<TA> a0 = av[base];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const double x = (double)a0.v[e];
+        const double y = to_d(v[base * VW + e]);
+        ca[0].add(x, y);
+        if (kAbs) ab[0] = __fma_rn(fabs(x), fabs(y), ab[0]);
+      }
+    }
+    for (int j = nv * VW + lane; j < n; j += 32) {
+      const double x = (double)arow[j];
+      const double y = to_d(v[j]);
+      ca[1].add(x, y);
+      if (kAbs) ab[1] = __fma_rn(fabs(x), fabs(y), ab[1]);
+    }
+    dd s = dd_add(dd_add(ca[0].get(), ca[1].get()), dd_add(ca[2].get(), ca[3].get()));
+    s = warp_sum_dd(s);
+    if (kAbs) *absdot = warp_sum((ab[0] + ab[1]) + (ab[2] + ab[3]));
+    return s;
+  }
   T acc[kU];
   double ab[kU];
 #pragma unroll

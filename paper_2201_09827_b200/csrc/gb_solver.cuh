@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -77,6 +78,10 @@ struct Prob {
   unsigned long long* ctr;    // [2]
   unsigned long long* epoch;  // [1]
   uint4* ytag = nullptr;      // tagged y of trsv_cta (2 x 16 B per entry)
+  int ytag_dsm = 0;           // > 0: ytag is the CTA's shared-memory copy (cluster of that many CTAs)
+  unsigned ytag_smem_off = 0;    // cluster launch: byte offset of the copy in dynamic smem
+  unsigned ytag_smem_bytes = 0;  // 0 = keep ytag in global memory
+  unsigned part_smem_off = 0;    // cluster launch: shared copy of the team partials (0 = none)
   GridCtl* ctl;
   double* partials;
   int kmax;
@@ -104,11 +109,34 @@ template <>
 struct MakeTeam<GridTeam> {
   template <class P>
   GB_DEVICE static GridTeam make(const P& p) {
-    return GridTeam{(int)gridDim.x, (int)blockIdx.x, p.ctl, p.partials, p.kmax, 0u};
+    return GridTeam{(int)gridDim.x, (int)blockIdx.x, p.ctl, p.partials, p.kmax, 0u,
+                    gridDim.x > 1 && cluster_ncta() == gridDim.x};
   }
 };
 
 __host__ __device__ inline size_t sm_doubles(int m, int k) { return (size_t)5 * m + 2 * k + 512; }
+
+// cluster team: move the tagged y of the CTA-per-block TRSV into shared memory
+// (zeroed here; the bodies' first team barrier orders it before any push).
+template <class Team, class P_t>
+__device__ void ytag_setup(Team& t, P_t& P, unsigned char* smem) {
+  if constexpr (Team::kGrid) {
+    if (t.clu && P.ytag_smem_bytes > 0) {
+      uint4* yt = reinterpret_cast<uint4*>(smem + P.ytag_smem_off);
+      for (unsigned i = threadIdx.x; i < P.ytag_smem_bytes / 16; i += blockDim.x) yt[i] = make_uint4(0u, 0u, 0u, 0u);
+      P.ytag = yt;
+      P.ytag_dsm = t.size();
+    }
+    if (t.clu && P.part_smem_off > 0) t.spart = reinterpret_cast<double*>(smem + P.part_smem_off);
+  }
+}
+// a CTA of the cluster must not exit while peers may still push into its copy
+template <class Team, class P_t>
+__device__ void ytag_finish(Team& t, const P_t& P) {
+  if constexpr (Team::kGrid) {
+    if (P.ytag_dsm > 0) t.sync();
+  }
+}
 
 template <class TW, class TF, int MV>
 __host__ __device__ inline size_t ops_bytes() {
@@ -127,6 +155,7 @@ __device__ void x0_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
   ts.ytag = P.ytag;
+  ts.dsm = P.ytag_dsm;
   double* red = sm + 4 * K.m + 4;
   t.sync();
   op_apply<UM>(t, K.sys, (const TW*)nullptr, P.b, P.xs, reinterpret_cast<typename Arith<UM>::T*>(K.ybuf), ts,
@@ -156,6 +185,7 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch, P.log};
   ts.ytag = P.ytag;
+  ts.dsm = P.ytag_dsm;
   mark(ts.log, 30);
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
@@ -216,6 +246,7 @@ __device__ void xref_refine_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void*
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
   ts.ytag = P.ytag;
+  ts.dsm = P.ytag_dsm;
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
   SysView<TW, double> sx{n,       K.sys.lda, K.sys.A,  K.sys.lda, P.LUx,    P.permx,
@@ -250,6 +281,7 @@ __device__ void debug_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops, 
   auto& K = P.K;
   TrsvSync ts{P.ctr, P.ctr + 1, *P.epoch};
   ts.ytag = P.ytag;
+  ts.dsm = P.ytag_dsm;
   double* red = sm + 4 * K.m + 4;
   const int n = K.n;
   int lo, hi;
@@ -281,7 +313,9 @@ __global__ void __launch_bounds__(kThreads) k_x0(Prob<TW, TF, MV> Pin) {
   Team t = MakeTeam<Team>::make(P);
   double* sm = reinterpret_cast<double*>(smem);
   void* ops = smem + sm_doubles(P.K.m, P.K.k) * sizeof(double);
+  ytag_setup(t, P, smem);
   x0_body(t, P, sm, ops);
+  ytag_finish(t, P);
 }
 
 template <class TW, class TF, int MV, class Team>
@@ -292,8 +326,10 @@ __global__ void __launch_bounds__(kThreads) k_step(Prob<TW, TF, MV> Pin) {
   double* sm = reinterpret_cast<double*>(smem);
   void* ops = smem + sm_doubles(P.K.m, P.K.k) * sizeof(double);
   P.K.fast = P.K.fast_cap > 0 ? reinterpret_cast<double*>(ops) : nullptr;
+  ytag_setup(t, P, smem);
   step_body(t, P, sm, ops);
   if (t.leader() && threadIdx.x == 0) P.K.keff_io[1] = (P.K.U == Pin.K.U) ? 0 : 1;
+  ytag_finish(t, P);
 }
 
 template <class TW, class TF, int MV, class Team>
@@ -303,7 +339,9 @@ __global__ void __launch_bounds__(kThreads) k_xref_refine(Prob<TW, TF, MV> Pin) 
   Team t = MakeTeam<Team>::make(P);
   double* sm = reinterpret_cast<double*>(smem);
   void* ops = smem + sm_doubles(P.K.m, P.K.k) * sizeof(double);
+  ytag_setup(t, P, smem);
   xref_refine_body(t, P, sm, ops);
+  ytag_finish(t, P);
 }
 
 template <int M, class TW, class TF, int MV, class Team>
@@ -313,7 +351,9 @@ __global__ void __launch_bounds__(kThreads) k_debug(Prob<TW, TF, MV> Pin, int wh
   Team t = MakeTeam<Team>::make(P);
   double* sm = reinterpret_cast<double*>(smem);
   void* ops = smem + sm_doubles(P.K.m, P.K.k) * sizeof(double);
+  ytag_setup(t, P, smem);
   debug_body<M>(t, P, sm, ops, what);
+  ytag_finish(t, P);
 }
 
 // dd GEPP xref (n <= 600) by one CTA
@@ -670,6 +710,27 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
 // ---------------------------------------------------------------------------
 // arena
 // ---------------------------------------------------------------------------
+// grow-only device buffers of the batched entry point (one pool per variant)
+struct BatchPool {
+  std::mutex mu;
+  void* ptr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t cap[5] = {0, 0, 0, 0, 0};
+  char* get(int i, size_t bytes) {
+    if (bytes > cap[i]) {
+      if (ptr[i]) cudaFree(ptr[i]);
+      ptr[i] = nullptr;
+      cap[i] = 0;
+      if (cudaMalloc(&ptr[i], bytes) != cudaSuccess) return nullptr;
+      cap[i] = bytes;
+    }
+    return reinterpret_cast<char*>(ptr[i]);
+  }
+};
+inline BatchPool& batch_pool() {
+  static BatchPool* p = new BatchPool();  // never destroyed: outlives the CUDA context teardown
+  return *p;
+}
+
 struct Arena {
   char* base = nullptr;
   size_t off = 0, cap = 0;
@@ -692,6 +753,7 @@ struct VariantOps;
 
 struct gb_solver {
   int n = 0, ldv = 0, lda = 0, G = 1;
+  bool cluster = false;  // the G-CTA team is launched as one thread-block cluster
   gb_options o{};
   cudaStream_t stream = nullptr;
   void* mem = nullptr;
@@ -821,6 +883,11 @@ struct Impl {
     P.ctr = s->ctr;
     P.epoch = s->epoch;
     P.ytag = s->ytag;
+    if (s->cluster) {
+      P.ytag_smem_off = (unsigned)((smem_bytes(s) + 15) & ~(size_t)15);
+      P.ytag_smem_bytes = (unsigned)(32 * (size_t)s->ldv);
+      P.part_smem_off = P.ytag_smem_off + P.ytag_smem_bytes;
+    }
     P.ctl = s->ctl;
     P.partials = s->partials;
     P.kmax = s->kmax;
@@ -844,7 +911,7 @@ struct Impl {
   static int fast_cap(int m, int k) {
     const size_t need = (size_t)leader_fast_need(m + k + 2, k) * sizeof(double);
     const size_t base = sm_doubles(m, k) * sizeof(double);
-    return (base + std::max(need, ops_bytes<TW, TF, MV>()) <= 200 * 1024) ? (int)(need / sizeof(double)) : 0;
+    return (base + std::max(need, ops_bytes<TW, TF, MV>()) <= 190 * 1024) ? (int)(need / sizeof(double)) : 0;
   }
   static size_t smem_bytes_for(int m, int k) {
     const int fc = fast_cap(m, k);
@@ -852,19 +919,70 @@ struct Impl {
   }
   static size_t smem_bytes(gb_solver* s) { return smem_bytes_for(s->o.m, s->o.k); }
 
+  // can G CTAs of this kernel (with `sm` bytes of smem each) run as one cluster?
+  template <class KernT>
+  static bool cluster_fits(gb_solver* s, KernT kern, size_t sm) {
+    if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(s->G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = s->G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclu = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclu, (const void*)kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return nclu >= 1;
+  }
+
   template <class KernT, class... Args>
   static gb_status launch(gb_solver* s, KernT kern, Args... args) {
     size_t sm = smem_bytes(s);
+    if (s->G == 1) {
+      gb_status st = set_smem(kern, sm);
+      if (st != GB_OK) return st;
+      count_launch();
+      kern<<<1, kThreads, sm, s->stream>>>(args...);
+      CK(cudaGetLastError());
+      return GB_OK;
+    }
+    // cluster team: + shared tagged y and the shared copy of the team
+    // partials (ytag_setup); otherwise the cooperative grid (the kernel sees
+    // no cluster and keeps both in global memory)
+    const size_t smc = ((sm + 15) & ~(size_t)15) + 32 * (size_t)s->ldv + 2 * sizeof(double) * s->G * s->kmax;
+    if (s->cluster && smc <= 227 * 1024 && set_smem(kern, smc) == GB_OK && cluster_fits(s, kern, smc)) {
+      count_launch();
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(s->G);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smc;
+      cfg.stream = s->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = s->G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, kern, args...));
+      return GB_OK;
+    }
+    cudaGetLastError();
     gb_status st = set_smem(kern, sm);
     if (st != GB_OK) return st;
     count_launch();
-    if (s->G == 1) {
-      kern<<<1, kThreads, sm, s->stream>>>(args...);
-      CK(cudaGetLastError());
-    } else {
-      void* argv[] = {(void*)&args...};
-      CK(cudaLaunchCooperativeKernel((void*)kern, dim3(s->G), dim3(kThreads), argv, sm, s->stream));
-    }
+    void* argv[] = {(void*)&args...};
+    CK(cudaLaunchCooperativeKernel((void*)kern, dim3(s->G), dim3(kThreads), argv, sm, s->stream));
     return GB_OK;
   }
 
@@ -1249,26 +1367,26 @@ struct Impl {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_batched<TW, TF, MV>, kThreads, sm));
     const int grid = std::max(1, std::min(count, sms * std::max(per, 1)));
-    // device buffers
-    char* slots = nullptr;
-    CK(cudaMalloc(&slots, Ly.stride * grid));
-    CK(cudaMemsetAsync(slots, 0, Ly.stride * grid, st));
+    // device buffers: a grow-only per-process pool (no cudaMalloc/cudaFree on
+    // the per-batch path once warm), guarded for concurrent callers
+    std::lock_guard<std::mutex> guard(batch_pool().mu);
     const size_t na = (size_t)count * n * n, nb = (size_t)count * n;
+    const size_t ints = (size_t)count * (5 + i_max) + 1, dbls = (size_t)count * (2 * i_max + n + 1);
+    char* slots = batch_pool().get(0, Ly.stride * grid);
+    int* ibuf = reinterpret_cast<int*>(batch_pool().get(1, sizeof(int) * ints));
+    double* dbuf = reinterpret_cast<double*>(batch_pool().get(2, sizeof(double) * dbls));
+    if (!slots || !ibuf || !dbuf) return fail(GB_ERR_CUDA, "batched workspace allocation failed");
+    CK(cudaMemsetAsync(slots, 0, Ly.stride * grid, st));
     const double *da = a, *db = b;
-    double *ta = nullptr, *tb = nullptr;
     if (!on_device) {
-      CK(cudaMalloc(&ta, sizeof(double) * na));
-      CK(cudaMalloc(&tb, sizeof(double) * nb));
+      double* ta = reinterpret_cast<double*>(batch_pool().get(3, sizeof(double) * na));
+      double* tb = reinterpret_cast<double*>(batch_pool().get(4, sizeof(double) * nb));
+      if (!ta || !tb) return fail(GB_ERR_CUDA, "batched input allocation failed");
       CK(cudaMemcpyAsync(ta, a, sizeof(double) * na, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(tb, b, sizeof(double) * nb, cudaMemcpyHostToDevice, st));
       da = ta;
       db = tb;
     }
-    const size_t ints = (size_t)count * (5 + i_max) + 1, dbls = (size_t)count * (2 * i_max + n + 1);
-    int* ibuf = nullptr;
-    double* dbuf = nullptr;
-    CK(cudaMalloc(&ibuf, sizeof(int) * ints));
-    CK(cudaMalloc(&dbuf, sizeof(double) * dbls));
     CK(cudaMemsetAsync(ibuf, 0, sizeof(int) * ints, st));
     BatchArgs A;
     A.count = count;
@@ -1324,11 +1442,6 @@ struct Impl {
     if (device_ms) *device_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaFree(slots);
-    cudaFree(ibuf);
-    cudaFree(dbuf);
-    if (ta) cudaFree(ta);
-    if (tb) cudaFree(tb);
     return GB_OK;
   }
 

@@ -59,6 +59,13 @@ struct CtaTeam {
   }
 };
 
+// number of CTAs in this thread-block cluster (1 without a cluster launch)
+GB_DEVICE unsigned cluster_ncta() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(v));
+  return v;
+}
+
 struct GridTeam {
   static constexpr bool kGrid = true;
   int G, r;
@@ -66,12 +73,23 @@ struct GridTeam {
   double* partials;  // 2 buffers of G * kMaxK doubles
   int kmax;
   unsigned phase;
+  // the whole team is one thread-block cluster (G <= 16 CTAs): sync() is the
+  // hardware cluster barrier (release/acquire at cluster scope) instead of
+  // the global-memory grid barrier
+  bool clu = false;
+  // cluster teams: per-CTA shared-memory copy of the partials buffers (same
+  // layout as `partials`); producers push their values into every CTA's copy
+  double* spart = nullptr;
 
   GB_DEVICE int size() const { return G; }
   GB_DEVICE int rank() const { return r; }
   GB_DEVICE bool leader() const { return r == 0; }
 
   __device__ void sync() {
+    if (clu) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      return;
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
       // the whole warp 0 spins uniformly (a lone spinning lane pays a large
@@ -102,10 +120,38 @@ struct GridTeam {
     hi = min(n, lo + per);
   }
   GB_DEVICE double* buf() { return partials + (size_t)(phase & 1) * G * kmax; }
+  GB_DEVICE double* sbuf() { return spart + (size_t)(phase & 1) * G * kmax; }
+  // store v at offset idx of the current shared buffer of cluster CTA q
+  GB_DEVICE static void push(double* local, int q, double v) {
+    unsigned ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(ra)
+                 : "r"((unsigned)__cvta_generic_to_shared(local)), "r"(q));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+  }
 
   // v[] holds this CTA's block-reduced values in every thread.
   template <class T, int K>
   __device__ void finish_sum(T (&v)[K]) {
+    if (spart != nullptr) {
+      // lane q of warp 0 pushes this CTA's K values into CTA q; the cluster
+      // barrier orders the pushes; then every CTA sums its local copy
+      double* p = sbuf();
+      if (threadIdx.x < G) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) push(p + (size_t)r * K + i, threadIdx.x, (double)v[i]);
+      }
+      sync();
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        T acc = T(0);
+        for (int g = lane; g < G; g += 32) acc += (T)p[(size_t)g * K + i];
+        v[i] = warp_sum(acc);
+      }
+      ++phase;
+      return;
+    }
     double* p = buf();
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -122,6 +168,18 @@ struct GridTeam {
     ++phase;
   }
   __device__ double finish_max(double v) {
+    if (spart != nullptr) {
+      double* p = sbuf();
+      if (threadIdx.x < G) push(p + r, threadIdx.x, v);
+      sync();
+      const int lane = threadIdx.x & 31;
+      double acc = -1.0;
+      for (int g = lane; g < G; g += 32) acc = nan_max(acc, p[g]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = nan_max(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      ++phase;
+      return acc;
+    }
     double* p = buf();
     if (threadIdx.x == 0) p[r] = v;
     sync();
@@ -136,6 +194,22 @@ struct GridTeam {
   // local[K] (smem, this CTA's partials) -> out[K] (smem) summed in rank order.
   template <class T>
   __device__ void sum_vec(const T* local, T* out, int K) {
+    if (spart != nullptr) {
+      double* p = sbuf();
+      for (int e = threadIdx.x; e < K * G; e += blockDim.x) {
+        const int i = e / G, q = e % G;
+        push(p + (size_t)r * K + i, q, (double)local[i]);
+      }
+      sync();
+      for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        T acc = T(0);
+        for (int g = 0; g < G; ++g) acc += (T)p[(size_t)g * K + i];
+        out[i] = acc;
+      }
+      __syncthreads();
+      ++phase;
+      return;
+    }
     double* p = buf();
     for (int i = threadIdx.x; i < K; i += blockDim.x) p[(size_t)r * K + i] = (double)local[i];
     sync();

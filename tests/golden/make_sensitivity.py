@@ -14,7 +14,16 @@ tests/test_oracle_golden.py) under these perturbations:
             combined by a tree (the GPU reduction shape), same format;
   lu     -- fp32/fp64 LU by an unblocked right-looking FMA-free elimination
             instead of LAPACK getrf (fp16 LU is exact on the GPU: unchanged);
-  both   -- the two together.
+  both   -- the two together;
+  op     -- the fp64 preconditioned operator (GEMV and both substitutions)
+            accumulated in 32 lane-strided partial sums combined by a tree
+            (the GPU's row-dot shape) instead of OpenBLAS dgemv/dtrsv order;
+  ulpS   -- the first refinement update x <- fl_u(x + nu d) moved by a
+            random {-1, 0, +1} ulp of u per entry (seed S = 0..7), later
+            updates exact: the iterate is stored at u, so any implementation
+            whose first correction differs in the last bit lands here.  On
+            the chaotic prolate rows this alone spans most of the envelope
+            (e.g. Table 6, alpha 0.45, GMRES-IR: step 2 in 29..32).
 
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_sensitivity.py
 """
@@ -34,7 +43,22 @@ sys.path.insert(0, ROOT)
 from oracle import cpu_gcrodr_ir as O  # noqa: E402
 from paper_2201_09827_b200 import problems  # noqa: E402
 
-_orig = {name: getattr(O, name) for name in ("vdot", "vnorm2", "tvec", "lu_factor")}
+_orig = {name: getattr(O, name) for name in ("vdot", "vnorm2", "tvec", "lu_factor", "apply_op", "precond_rhs",
+                                               "vadd")}
+_ULP = {"rng": None}
+
+
+def vadd_ulp(x, y, fmt):
+    """The refinement update (only caller of vadd) with a last-bit perturbation."""
+    s = _orig["vadd"](x, y, fmt)
+    if _ULP["rng"] is None or fmt not in (O.SINGLE, O.DOUBLE):
+        return s
+    rng, _ULP["rng"] = _ULP["rng"], None  # first update of the solve only
+    dt = np.float32 if fmt == O.SINGLE else np.float64
+    f = s.astype(dt)
+    d = rng.integers(-1, 2, size=f.shape)
+    f = np.where(d > 0, np.nextafter(f, dt(np.inf)), np.where(d < 0, np.nextafter(f, dt(-np.inf)), f))
+    return f.astype(np.float64)
 
 
 def _lane_sum(prod: np.ndarray, dt) -> float:
@@ -110,23 +134,73 @@ def lu_unblocked(a, fmt):
     return O.Factors(np.tril(w, -1) + np.eye(n), upper, perm, fmt, float(np.max(np.abs(upper)) / amax))
 
 
-def _set(lanes: bool, lu: bool):
+def _rows_lanes(m: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """fp64 row dots m @ x in 32 lane-strided partial sums + a tree."""
+    n = m.shape[1]
+    pad = (-n) % 32
+    p = np.concatenate([m * x[None, :], np.zeros((m.shape[0], pad))], axis=1).reshape(m.shape[0], -1, 32)
+    acc = np.zeros((m.shape[0], 32))
+    for c in range(p.shape[1]):
+        acc = acc + p[:, c, :]
+    while acc.shape[1] > 1:
+        acc = acc[:, 0::2] + acc[:, 1::2]
+    return acc[:, 0]
+
+
+def _sub_rows(f, y):
+    y = y.copy()
+    n = f.n
+    for i in range(1, n):
+        y[i] = y[i] - _rows_lanes(f.L[i:i + 1, :i], y[:i])[0]
+    for i in range(n - 1, -1, -1):
+        if i < n - 1:
+            y[i] = y[i] - _rows_lanes(f.U[i:i + 1, i + 1:], y[i + 1:])[0]
+        y[i] = y[i] / f.U[i, i]
+    return y
+
+
+def apply_op_lanes(a, f, v, fmt, store):
+    if fmt != O.DOUBLE:
+        return _orig["apply_op"](a, f, v, fmt, store)
+    w = _rows_lanes(np.asarray(a, dtype=np.float64), np.asarray(v, dtype=np.float64))
+    return O.rnd(_sub_rows(f, w[f.perm]), store)
+
+
+def precond_rhs_lanes(f, r, fmt, store):
+    if fmt != O.DOUBLE:
+        return _orig["precond_rhs"](f, r, fmt, store)
+    return O.rnd(_sub_rows(f, np.asarray(r, dtype=np.float64)[f.perm]), store)
+
+
+def _set(lanes: bool, lu: bool, op: bool = False, ulp_seed=None):
+    _ULP["rng"] = None if ulp_seed is None else np.random.default_rng(ulp_seed)
+    O.vadd = vadd_ulp if ulp_seed is not None else _orig["vadd"]
+    O.apply_op = apply_op_lanes if op else _orig["apply_op"]
+    O.precond_rhs = precond_rhs_lanes if op else _orig["precond_rhs"]
     O.vdot = vdot_lanes if lanes else _orig["vdot"]
     O.vnorm2 = vnorm2_lanes if lanes else _orig["vnorm2"]
     O.tvec = tvec_lanes if lanes else _orig["tvec"]
     O.lu_factor = lu_unblocked if lu else _orig["lu_factor"]
 
 
-def envelope(a, b, prec, method, m, k, tau, i_max):
+def squared_fmt(u: str) -> str:
+    return O.squared(u)
+
+
+def envelope(a, b, prec, method, m, k, tau, i_max, ulp=True):
     runs = {}
     variants = {"ref": (False, False, "lanes"), "lanes": (True, False, "lanes"), "lu": (False, True, "lanes"),
                 "both": (True, True, "lanes"), "reversed": (True, False, "reversed"),
-                "wide": (True, False, "wide")}
+                "wide": (True, False, "wide"), "op": (False, False, "op"), "op+lanes": (True, False, "op+lanes")}
+    if ulp:
+        variants.update({f"ulp{sd}": (False, False, f"ulp{sd}") for sd in range(8)})
     for name, (lanes, lu, order) in variants.items():
         if lu and prec[0] == "half":
             continue
-        _MODE["order"] = order
-        _set(lanes, lu)
+        if order.startswith("op") and squared_fmt(prec[1]) != O.DOUBLE:
+            continue
+        _MODE["order"] = order if order in ("lanes", "reversed", "wide") else "lanes"
+        _set(lanes, lu, op=order.startswith("op"), ulp_seed=int(order[3:]) if order.startswith("ulp") else None)
         try:
             rep = O.solve(a, b, tuple(prec), method, m, k, tau, i_max)
             runs[name] = {"inner": rep.inner_iters, "converged": rep.converged,
@@ -190,7 +264,21 @@ def main():
 if __name__ == "__main__":
     if os.environ.get("OPENBLAS_NUM_THREADS") != "1":
         sys.exit("set OPENBLAS_NUM_THREADS=1")
-    if "--lu-only" in sys.argv:
+    if "--tables-only" in sys.argv:
+        path = os.path.join(HERE, "sensitivity.json")
+        data = json.load(open(path))
+        data["tables"] = []
+        for tab in ("table5", "table6"):
+            for row in json.load(open(os.path.join(HERE, f"{tab}.json")))["rows"]:
+                a = problems.prolate(100, row["alpha"])
+                env = envelope(a, np.ones(100), row["precisions"], row["method"], row["m"], row["k"],
+                               row["tau"], row["i_max"])
+                env.update({"table": tab, "alpha": row["alpha"], "method": row["method"]})
+                data["tables"].append(env)
+                print(tab, row["alpha"], row["method"], {k: v["inner"][:4] for k, v in env["runs"].items()},
+                      flush=True)
+        json.dump(data, open(path, "w"), indent=0)
+    elif "--lu-only" in sys.argv:
         path = os.path.join(HERE, "sensitivity.json")
         data = json.load(open(path))
         main_lu(data)

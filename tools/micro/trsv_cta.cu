@@ -14,17 +14,24 @@ __global__ void __launch_bounds__(256) k_trsv(int n, const float* LU, size_t ld,
                                               double* partials, unsigned long long* tout, const double* ih,
                                               const double* il, unsigned long long* stamps, uint4* yt) {
   extern __shared__ __align__(16) unsigned char smem[];
-  GridTeam t{(int)gridDim.x, (int)blockIdx.x, ctl, partials, 64, 0u};
+  GridTeam t{(int)gridDim.x, (int)blockIdx.x, ctl, partials, 64, 0u, gridDim.x > 1 && cluster_ncta() == gridDim.x};
   TrsvSync ts{ctr, ctr + 1, epoch, PhaseLog{nullptr, 0}, stamps, yt};
+  if (t.clu) {  // tagged y in cluster shared memory (after the TRSV tiles)
+    uint4* loc = reinterpret_cast<uint4*>(smem + 8 * 32 * 33 * sizeof(double) + 256 * 16);
+    for (int i = threadIdx.x; i < 2 * n; i += blockDim.x) loc[i] = yt[i];  // same initial tags
+    ts.ytag = loc;
+    ts.dsm = t.size();
+  }
   t.sync();
   unsigned long long t0 = gtimer();
   trsv_cta<M, GridTeam, float, kLower>(t, n, LU, ld, y, ts, smem, ih, il);
   t.sync();
+  if (t.clu && (stamps != nullptr)) {}
   if (blockIdx.x == 0 && threadIdx.x == 0) tout[0] = gtimer() - t0;
 }
 
 template <int M, bool kLower>
-float run(int n, int G, bool stamps_out) {
+float run(int n, int G, bool stamps_out, bool clu = false) {
   using T = typename Arith<M>::T;
   size_t ld = (n + 31) & ~31;
   int nb = (n + 31) / 32;
@@ -57,7 +64,7 @@ float run(int n, int G, bool stamps_out) {
   cudaMemset(yt, 0, 32 * (size_t)n);
   cudaMalloc(&stamps, 8 * 3 * nb);
   cudaMemset(stamps, 0, 8 * 3 * nb);
-  size_t sm = 8 * 32 * 33 * sizeof(double);
+  size_t sm = 8 * 32 * 33 * sizeof(double) + 256 * 16 + (clu ? 32 * (size_t)n : 0);
   auto kern = k_trsv<M, kLower>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   unsigned long long epoch = 0, hout = 0;
@@ -70,7 +77,24 @@ float run(int n, int G, bool stamps_out) {
       cudaMemcpy(yt, w.data(), 4 * w.size(), cudaMemcpyHostToDevice);
     }
     void* args[] = {&n, &LU, &ld, &y, &ctr, &epoch, &ctl, &part, &tout, &ih, &il, &stamps, &yt};
-    cudaLaunchCooperativeKernel((void*)kern, G, 256, args, sm, 0);
+    if (clu) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = sm;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kern, n, (const float*)LU, ld, y, ctr, epoch, ctl, part, tout, (const double*)ih,
+                         (const double*)il, stamps, yt);
+    } else {
+      cudaLaunchCooperativeKernel((void*)kern, G, 256, args, sm, 0);
+    }
     cudaDeviceSynchronize();
     cudaMemcpy(&hout, tout, 8, cudaMemcpyDeviceToHost);
     best = std::min(best, hout / 1e3f);
@@ -103,6 +127,20 @@ int main() {
              run<MODE_DD, false>(n, G, false));
     }
   }
+  for (int G : {8, 16}) {
+    printf("cluster n 1024 G %d: f64 fwd %8.1f us bwd %8.1f us | dd fwd %8.1f us bwd %8.1f us\n", G,
+           run<MODE_F64, true>(1024, G, false, true), run<MODE_F64, false>(1024, G, false, true),
+           run<MODE_DD, true>(1024, G, false, true), run<MODE_DD, false>(1024, G, false, true));
+    printf("grid    n 1024 G %d: f64 fwd %8.1f us bwd %8.1f us | dd fwd %8.1f us bwd %8.1f us\n", G,
+           run<MODE_F64, true>(1024, G, false, false), run<MODE_F64, false>(1024, G, false, false),
+           run<MODE_DD, true>(1024, G, false, false), run<MODE_DD, false>(1024, G, false, false));
+  }
+  printf("dd fwd n=1024 G=16 cluster:\n");
+  run<MODE_DD, true>(1024, 16, true, true);
+  printf("dd bwd n=1024 G=16 cluster:\n");
+  run<MODE_DD, false>(1024, 16, true, true);
+  printf("f64 fwd n=1024 G=16 cluster:\n");
+  run<MODE_F64, true>(1024, 16, true, true);
   printf("dd fwd n=1024 G=32:\n");
   run<MODE_DD, true>(1024, 32, true);
   printf("dd fwd n=8192 G=148:\n");
