@@ -104,7 +104,10 @@ static __device__ __noinline__ int blk_getrf(double* a, int ld, int p, int* piv)
   return zero;
 }
 
-// B (p x q) <- A^-1 B using blk_getrf factors; one thread per column of B.
+// B (p x q) <- A^-1 B using blk_getrf factors.  The row interchanges run one
+// thread per column; the substitutions sweep j in order with every (row,
+// column) update of a step in parallel, so each element sees the same
+// operation sequence as a per-column column-sweep solve.
 static __device__ __noinline__ void blk_getrs(const double* a, int ld, int p, const int* piv, double* b, int ldb,
                                  int q) {
   for (int c = threadIdx.x; c < q; c += blockDim.x) {
@@ -117,20 +120,31 @@ static __device__ __noinline__ void blk_getrs(const double* a, int ld, int p, co
         x[pk] = t;
       }
     }
-    for (int j = 0; j < p; ++j) {
-      double xj = x[j];
-      if (xj != 0.0)
-        for (int i = j + 1; i < p; ++i) x[i] = __fma_rn(-xj, a[IX(i, j, ld)], x[i]);
-    }
-    for (int j = p - 1; j >= 0; --j) {
-      if (x[j] != 0.0) {
-        x[j] = x[j] / a[IX(j, j, ld)];
-        double xj = x[j];
-        for (int i = 0; i < j; ++i) x[i] = __fma_rn(-xj, a[IX(i, j, ld)], x[i]);
-      }
-    }
   }
   __syncthreads();
+  // forward (unit lower)
+  for (int j = 0; j < p - 1; ++j) {
+    const int m = p - 1 - j;
+    for (int e = threadIdx.x; e < m * q; e += blockDim.x) {
+      const int i = j + 1 + e % m, c = e / m;
+      const double xj = b[IX(j, c, ldb)];
+      if (xj != 0.0) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
+    }
+    __syncthreads();
+  }
+  // backward (upper)
+  for (int j = p - 1; j >= 0; --j) {
+    for (int c = threadIdx.x; c < q; c += blockDim.x)
+      if (b[IX(j, c, ldb)] != 0.0) b[IX(j, c, ldb)] = b[IX(j, c, ldb)] / a[IX(j, j, ld)];
+    __syncthreads();
+    if (j == 0) break;
+    for (int e = threadIdx.x; e < j * q; e += blockDim.x) {
+      const int i = e % j, c = e / j;
+      const double xj = b[IX(j, c, ldb)];
+      if (xj != 0.0) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------

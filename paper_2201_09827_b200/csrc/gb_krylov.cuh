@@ -20,6 +20,10 @@
 
 namespace gb {
 
+// leader-only orthogonalisation for n <= kLeaderOrthRows (w in registers)
+constexpr int kThreadsPerCta = 256;
+constexpr int kLeaderOrthRows = 2048;
+
 // status bits reported per inner solve
 enum : int { KS_CONVERGED = 1, KS_STAGNATED = 2, KS_BREAKDOWN = 4 };
 
@@ -143,6 +147,155 @@ struct CycleOut {
   bool converged, breakdown;
 };
 
+// Givens update of column j (gmres.py:99-114, 182-190) by thread 0: each
+// product and sum rounded to u.  col[0..j+1] in, rotated column in rot.
+template <class TW>
+GB_DEVICE void givens_update(int j, const double* col, double* rot, double* cs, double* sn, double* g) {
+  using F = Fmt<TW>;
+  for (int i = 0; i <= j + 1; ++i) rot[i] = col[i];
+  for (int i = 0; i < j; ++i) {
+    double a = rot[i], b = rot[i + 1];
+    rot[i] = F::rnd(F::rnd(cs[i] * a) + F::rnd(sn[i] * b));
+    rot[i + 1] = F::rnd(F::rnd(cs[i] * b) - F::rnd(sn[i] * a));
+  }
+  double hh = hypot(rot[j], rot[j + 1]);
+  double c = 1.0, s2 = 0.0;
+  if (hh != 0.0) {
+    c = F::rnd(rot[j] / hh);
+    s2 = F::rnd(rot[j + 1] / hh);
+  }
+  cs[j] = c;
+  sn[j] = s2;
+  rot[j] = F::rnd(F::rnd(c * rot[j]) + F::rnd(s2 * rot[j + 1]));
+  rot[j + 1] = 0.0;
+  double gj = g[j];
+  g[j] = F::rnd(F::rnd(c * gj) + F::rnd(s2 * 0.0));
+  g[j + 1] = F::rnd(F::rnd(c * 0.0) - F::rnd(s2 * gj));
+}
+
+// spare broadcast slots after the recycle matrices in K.bc (64 doubles)
+template <class TW, class TA, class TF, int MV>
+GB_DEVICE double* bc_orth(const Krylov<TW, TA, TF, MV>& K) {
+  const size_t S = (size_t)K.m + K.k + 2;
+  return K.bc + 3 * S + 2 * S * (K.k + 2) + 2 * (size_t)(K.k + 1) * (K.k + 1);
+}
+
+// block-wide sum of this thread's partial (all threads get it)
+template <class A>
+GB_DEVICE A blk_sum1(A v, double* red) {
+  A a[1] = {v};
+  block_sum<A, 1>(a, reinterpret_cast<A*>(red));
+  return a[0];
+}
+
+// Leader-only orthogonalisation of w against C (one CGS projection) and V
+// (MGS with selective reorthogonalisation), the Givens update and the next
+// basis vector -- the whole of gmres.py:150-201 for one step, run by the
+// leader CTA over all n <= kLeaderOrthRows rows.  w lives in registers (QW
+// rows per thread) and the next basis column is loaded into registers before
+// each block reduction, so every dot costs one block reduction and no team
+// barrier: a step takes two team barriers instead of j + 4.  Results through
+// bc_orth: [0] = ||w|| after orthogonalisation, [1] = |g_{j+1}|.
+template <class TW, class TA, class TF, int MV>
+__device__ __noinline__ void leader_orth(Krylov<TW, TA, TF, MV>& K, int j, int kc, double* cs, double* sn, double* g,
+                            double* col, double* red, double* tmp) {
+  using F = Fmt<TW>;
+  using Acc = typename F::Acc;
+  constexpr int QW = kLeaderOrthRows / kThreadsPerCta;
+  const int n = K.n, ldv = K.ldv, M = K.m;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  TW wr[QW], cur[QW], prv[QW];
+  auto ld_col = [&](const TW* base, TW (&d)[QW]) {
+#pragma unroll
+    for (int q = 0; q < QW; ++q) {
+      const int r = tid + q * bd;
+      d[q] = r < n ? base[r] : TW(0);
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < QW; ++q) {
+    const int r = tid + q * bd;
+    wr[q] = r < n ? __ldcg(K.w + r) : TW(0);
+  }
+  if (kc > 0) {
+    // cc = C^T w (each dot in the work format), then w -= cc_i C_i in order
+    ld_col(K.C, cur);
+    for (int i = 0; i < kc; ++i) {
+      Acc a = Acc(0);
+#pragma unroll
+      for (int q = 0; q < QW; ++q) a = F::mac(a, cur[q], wr[q]);
+      if (i + 1 < kc) ld_col(K.C + (size_t)(i + 1) * ldv, cur);
+      a = blk_sum1<Acc>(a, red);
+      if (tid == 0) tmp[i] = (double)a;
+    }
+    __syncthreads();
+    for (int i = 0; i < kc; ++i) {
+      ld_col(K.C + (size_t)i * ldv, cur);
+      const double ci = tmp[i];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) wr[q] = F::axpy(-ci, cur[q], wr[q]);
+    }
+    for (int i = tid; i < kc; i += bd) K.B[IX(i, j, K.k + 1)] = tmp[i];
+    __syncthreads();
+  }
+  auto nrm2 = [&]() {
+    Acc a = Acc(0);
+#pragma unroll
+    for (int q = 0; q < QW; ++q) a = F::mac(a, wr[q], wr[q]);
+    return F::sqrt_((double)blk_sum1<Acc>(a, red));
+  };
+  const double wnorm0 = nrm2();
+  // MGS: h_i = v_i . w ; w -= h_i v_i  (axpy fused with the next dot)
+  auto mgs = [&](bool accumulate) {
+    double hprev = 0.0;
+    ld_col(K.V, cur);
+    for (int i = 0; i <= j; ++i) {
+      Acc a = Acc(0);
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        if (i > 0) wr[q] = F::axpy(-hprev, prv[q], wr[q]);
+        a = F::mac(a, cur[q], wr[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < QW; ++q) prv[q] = cur[q];
+      if (i < j) ld_col(K.V + (size_t)(i + 1) * ldv, cur);
+      hprev = (double)blk_sum1<Acc>(a, red);
+      if (tid == 0) col[i] = accumulate ? F::rnd(col[i] + hprev) : hprev;
+    }
+#pragma unroll
+    for (int q = 0; q < QW; ++q) wr[q] = F::axpy(-hprev, prv[q], wr[q]);
+  };
+  mgs(false);
+  double hlast = nrm2();
+  if (K.reorth && hlast < sqrt(F::u) * wnorm0) {
+    mgs(true);
+    hlast = nrm2();
+  }
+  if (tid == 0) {
+    col[j + 1] = hlast;
+    givens_update<TW>(j, col, tmp, cs, sn, g);
+  }
+  __syncthreads();
+  for (int i = tid; i <= j + 1; i += bd) {
+    K.H[IX(i, j, M + 1)] = col[i];
+    K.R[IX(i, j, M + 1)] = tmp[i];
+  }
+  if (hlast != 0.0) {
+    TW* vn = K.V + (size_t)(j + 1) * ldv;
+    const double rh = 1.0 / hlast;
+#pragma unroll
+    for (int q = 0; q < QW; ++q) {
+      const int r = tid + q * bd;
+      if (r < n) vn[r] = F::scale(rh, wr[q]);
+    }
+  }
+  if (tid == 0) {
+    double* o = bc_orth(K);
+    o[0] = hlast;
+    o[1] = fabs(g[j + 1]);
+  }
+}
+
 template <class TW, class TA, class TF, int MV, class Team>
 __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& ts, const TW* r0,
                                   double beta, int mb, double tol_abs, int kc, bool want_y,
@@ -165,6 +318,24 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
     TW* vj = colp(K.V, ldv, j);
     mark(ts.log, 20);
     apply_A(t, K, ts, vj, K.w, smem_ops, applies);
+    if (Team::kGrid && n <= kLeaderOrthRows && blockDim.x == kThreadsPerCta) {
+      t.sync();  // w complete
+      if (t.leader()) leader_orth(K, j, kc, cs, sn, g, col, red, tmp);
+      t.sync();
+      const double* o = bc_orth(K);
+      const double hlast = __ldcg(o), estimate = __ldcg(o + 1);
+      co.steps = j + 1;
+      mark(ts.log, 25);
+      if (hlast == 0.0) {
+        co.breakdown = co.converged = true;
+        break;
+      }
+      if (estimate <= tol_abs) {
+        co.converged = true;
+        break;
+      }
+      continue;
+    }
     // deflation against C: one CGS projection, sequential subtraction
     if (kc > 0) {
       team_tvec2<TW>(t, K.C, kc, (const TW*)nullptr, 0, ldv, K.w, n, tmp, red);
@@ -180,28 +351,46 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
     mark(ts.log, 21);
     const double wnorm0 = team_nrm2<TW>(t, K.w, n, red);
     mark(ts.log, 22);
-    // MGS: h_i = v_i . w ; w -= h_i v_i  (axpy fused with the next dot)
+    // MGS: h_i = v_i . w ; w -= h_i v_i  (axpy fused with the next dot).
+    // This thread's rows of w stay in registers for the whole sweep and the
+    // next basis column is loaded before each reduction (the loads do not
+    // depend on it), so one team reduction is the only latency per i.
     double hprev = 0.0;
-    for (int i = 0; i <= j; ++i) {
-      const TW* vi = colp(K.V, ldv, i);
-      const TW* vp = i > 0 ? colp(K.V, ldv, i - 1) : nullptr;
-      typename F::Acc a[1] = {typename F::Acc(0)};
-      for (int r = lo + threadIdx.x; r < hi; r += blockDim.x) {
-        TW wr = K.w[r];
-        if (i > 0) {
-          wr = F::axpy(-hprev, vp[r], wr);
-          K.w[r] = wr;
-        }
-        a[0] = F::mac(a[0], vi[r], wr);
-      }
-      block_sum<typename F::Acc, 1>(a, reinterpret_cast<typename F::Acc*>(red));
-      t.template finish_sum<typename F::Acc, 1>(a);
-      hprev = (double)a[0];
-      if (threadIdx.x == 0) col[i] = hprev;
-    }
     {
-      const TW* vp = colp(K.V, ldv, j);
-      for (int r = lo + threadIdx.x; r < hi; r += blockDim.x) K.w[r] = F::axpy(-hprev, vp[r], K.w[r]);
+      constexpr int QW = 4;  // rows per thread: a CTA slice has <= 4 * blockDim rows
+      TW wr[QW], vc[QW], vn[QW];
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        const int r = lo + threadIdx.x + q * blockDim.x;
+        wr[q] = r < hi ? K.w[r] : TW(0);
+        vc[q] = r < hi ? K.V[r] : TW(0);
+      }
+      for (int i = 0; i <= j; ++i) {
+        typename F::Acc a[1] = {typename F::Acc(0)};
+#pragma unroll
+        for (int q = 0; q < QW; ++q) {
+          const int r = lo + threadIdx.x + q * blockDim.x;
+          if (r < hi) {
+            if (i > 0) wr[q] = F::axpy(-hprev, vn[q], wr[q]);  // vn = v_{i-1}
+            a[0] = F::mac(a[0], vc[q], wr[q]);
+          }
+        }
+        // v_{i-1} <- v_i ; prefetch v_{i+1}
+#pragma unroll
+        for (int q = 0; q < QW; ++q) {
+          const int r = lo + threadIdx.x + q * blockDim.x;
+          vn[q] = vc[q];
+          vc[q] = (r < hi && i < j) ? K.V[(size_t)(i + 1) * ldv + r] : TW(0);
+        }
+        t.template reduce<typename F::Acc, 1>(a, reinterpret_cast<typename F::Acc*>(red));
+        hprev = (double)a[0];
+        if (threadIdx.x == 0) col[i] = hprev;
+      }
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        const int r = lo + threadIdx.x + q * blockDim.x;
+        if (r < hi) K.w[r] = F::axpy(-hprev, vn[q], wr[q]);  // vn = v_j
+      }
     }
     mark(ts.log, 23);
     double hlast = team_nrm2<TW>(t, K.w, n, red);
@@ -219,8 +408,7 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
           }
           a[0] = F::mac(a[0], vi[r], wr);
         }
-        block_sum<typename F::Acc, 1>(a, reinterpret_cast<typename F::Acc*>(red));
-        t.template finish_sum<typename F::Acc, 1>(a);
+        t.template reduce<typename F::Acc, 1>(a, reinterpret_cast<typename F::Acc*>(red));
         hprev = (double)a[0];
         if (threadIdx.x == 0) col[i] = F::rnd(col[i] + hprev);
       }
@@ -231,27 +419,7 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
     __syncthreads();
     if (threadIdx.x == 0) {
       col[j + 1] = hlast;
-      // Givens (gmres.py:99-114, 182-190): each product and sum rounded to u
-      double* rot = tmp;
-      for (int i = 0; i <= j + 1; ++i) rot[i] = col[i];
-      for (int i = 0; i < j; ++i) {
-        double a = rot[i], b = rot[i + 1];
-        rot[i] = F::rnd(F::rnd(cs[i] * a) + F::rnd(sn[i] * b));
-        rot[i + 1] = F::rnd(F::rnd(cs[i] * b) - F::rnd(sn[i] * a));
-      }
-      double hh = hypot(rot[j], rot[j + 1]);
-      double c = 1.0, s2 = 0.0;
-      if (hh != 0.0) {
-        c = F::rnd(rot[j] / hh);
-        s2 = F::rnd(rot[j + 1] / hh);
-      }
-      cs[j] = c;
-      sn[j] = s2;
-      rot[j] = F::rnd(F::rnd(c * rot[j]) + F::rnd(s2 * rot[j + 1]));
-      rot[j + 1] = 0.0;
-      double gj = g[j];
-      g[j] = F::rnd(F::rnd(c * gj) + F::rnd(s2 * 0.0));
-      g[j + 1] = F::rnd(F::rnd(c * 0.0) - F::rnd(s2 * gj));
+      givens_update<TW>(j, col, tmp, cs, sn, g);
     }
     __syncthreads();
     if (t.leader()) {
@@ -772,44 +940,83 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
   }
   __syncthreads();
   if (s_flag) return -1;  // NoConvergence / SingularB propagate -> keep space
-  // shared-memory staging when it fits (the eigen iteration and the
-  // bidiagonalisation are latency bound: every scalar step touches the matrix)
+  // shared-memory staging when it fits (the factorisation, the eigen
+  // iteration and the bidiagonalisation are latency bound: every scalar step
+  // touches the matrix).  fast layout: [emat p^2 | lu p^2 | inv p^2 | ...]
   const bool fast = K.fast != nullptr && leader_fast_need(gc, kk) <= K.fast_cap;
-  double* cmat = fast ? K.fast : b1c;
-  for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) cmat[e] = b1[e];
+  const size_t pp = (size_t)gc * gc;
+  double* emat = fast ? K.fast : rd;        // b1^-1 a1 (eig input)
+  double* lu = fast ? K.fast + pp : b1;     // LU factors of b1
+  double* escr = fast ? K.fast + pp : scr;  // eig scratch (after the solves)
+  for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) {
+    emat[e] = a1[e];
+    if (fast) lu[e] = b1[e];
+  }
   __syncthreads();
   mark(lg, 60);
-  double cnd = blk_cond2(cmat, gc, gc, bd, scr);
-  mark(lg, 61);
-  if (!(cnd <= 1.0 / kEps53)) {
-    // shift by sqrt(u) * ||b1||_F and retry once (gcrodr.py:192-196)
-    double f = 0.0;
-    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) f = __fma_rn(b1[e], b1[e], f);
-    double ff[1] = {f};
-    block_sum<double, 1>(ff, s_red);
-    const double shift = sqrt(kEps53) * sqrt(ff[0]);
-    for (int e = threadIdx.x; e < gc; e += blockDim.x) b1[IX(e, e, gc)] += shift;
+  // SingularB screen (eig_generalized, densela.py:460-477: cond2(b1) > 2^53).
+  // cond2 <= p * cond1, so an exactly computed ||b1||_1 ||b1^-1||_1 below
+  // 2^53 / (4 p) proves the pencil regular without the SVD; otherwise (and
+  // without the fast staging) the 2-norm condition number decides.
+  bool need_cond2 = true;
+  int zero = fast ? blk_getrf(lu, gc, gc, piv) : -1;
+  if (fast && zero < 0) {
+    double* inv = K.fast + 2 * pp;
+    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) inv[e] = (e % gc == e / gc) ? 1.0 : 0.0;
     __syncthreads();
+    blk_getrs(lu, gc, gc, piv, inv, gc, gc);
+    __shared__ double s_n1[2];
+    if (threadIdx.x < 64) {
+      const int lane = threadIdx.x & 31;
+      // column sums: warp 0 over b1, warp 1 over the inverse
+      const double* m = threadIdx.x < 32 ? b1 : inv;
+      double best = 0.0;
+      for (int c = lane; c < gc; c += 32) {
+        double cs = 0.0;
+        for (int r0 = 0; r0 < gc; ++r0) cs += fabs(m[IX(r0, c, gc)]);
+        best = nan_max(best, cs);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = nan_max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (lane == 0) s_n1[threadIdx.x >> 5] = best;
+    }
+    __syncthreads();
+    const double c1 = s_n1[0] * s_n1[1];
+    need_cond2 = !(c1 * 4.0 * gc < 1.0 / kEps53);
+    __syncthreads();
+  }
+  if (need_cond2) {
+    double* cmat = fast ? K.fast + 2 * pp : b1c;
     for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) cmat[e] = b1[e];
     __syncthreads();
-    cnd = blk_cond2(cmat, gc, gc, bd, scr);
-    if (!(cnd <= 1.0 / kEps53)) return -1;
+    double cnd = blk_cond2(cmat, gc, gc, bd, scr);
+    if (!(cnd <= 1.0 / kEps53)) {
+      // shift by sqrt(u) * ||b1||_F and retry once (gcrodr.py:192-196)
+      double f = 0.0;
+      for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) f = __fma_rn(b1[e], b1[e], f);
+      double ff[1] = {f};
+      block_sum<double, 1>(ff, s_red);
+      const double shift = sqrt(kEps53) * sqrt(ff[0]);
+      for (int e = threadIdx.x; e < gc; e += blockDim.x) b1[IX(e, e, gc)] += shift;
+      __syncthreads();
+      for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) cmat[e] = b1[e];
+      __syncthreads();
+      cnd = blk_cond2(cmat, gc, gc, bd, scr);
+      if (!(cnd <= 1.0 / kEps53)) return -1;
+      // refactor the shifted pencil
+      for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) lu[e] = b1[e];
+      __syncthreads();
+      zero = blk_getrf(lu, gc, gc, piv);
+    } else if (!fast) {
+      zero = blk_getrf(lu, gc, gc, piv);  // lu == b1 (cond2 worked on a copy)
+    }
   }
+  mark(lg, 61);
   // reduced = b1^-1 a1
-  for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) rd[e] = a1[e];
-  __syncthreads();
-  if (blk_getrf(b1, gc, gc, piv) >= 0) return -1;
+  if (zero >= 0) return -1;
   mark(lg, 62);
-  blk_getrs(b1, gc, gc, piv, rd, gc, gc);
+  blk_getrs(lu, gc, gc, piv, emat, gc, gc);
   mark(lg, 63);
-  double* emat = rd;
-  double* escr = scr;
-  if (fast) {
-    emat = K.fast;
-    escr = K.fast + (size_t)gc * gc;
-    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) emat[e] = rd[e];
-    __syncthreads();
-  }
   const int kn = leader_ritz_basis(emat, gc, kk, P, gc, escr);
   mark(lg, 64);
   if (kn <= 0) return -1;

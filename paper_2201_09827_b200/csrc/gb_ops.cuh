@@ -1062,8 +1062,7 @@ __device__ void team_dots(Team& t, const TW* const (&x)[K], const TW* y, int n, 
 #pragma unroll
     for (int i = 0; i < K; ++i) a[i] = Fmt<TW>::mac(a[i], x[i][j], yj);
   }
-  block_sum<Acc, K>(a, reinterpret_cast<Acc*>(red));
-  t.template finish_sum<Acc, K>(a);
+  t.template reduce<Acc, K>(a, reinterpret_cast<Acc*>(red));
 #pragma unroll
   for (int i = 0; i < K; ++i) out[i] = (double)a[i];
 }

@@ -50,6 +50,11 @@ struct CtaTeam {
   // them team-wide.  Nothing to do for a single CTA.
   template <class T, int K>
   GB_DEVICE void finish_sum(T (&v)[K]) {}
+  // every thread holds its partials; on return every thread holds the team sums
+  template <class T, int K>
+  __device__ void reduce(T (&v)[K], T* scratch) {
+    block_sum<T, K>(v, scratch);
+  }
   GB_DEVICE double finish_max(double v) { return v; }
   // vector variant: local[K] in smem (this CTA's partials) -> out[K] in smem
   template <class T>
@@ -128,6 +133,36 @@ struct GridTeam {
                  : "=r"(ra)
                  : "r"((unsigned)__cvta_generic_to_shared(local)), "r"(q));
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+  }
+
+  // every thread holds its partials; on return every thread of every CTA
+  // holds the team sums (bit-identical: fixed summation order).  Cluster
+  // teams skip the block reduction: each warp pushes its warp sum straight
+  // into every CTA's shared copy and one cluster barrier publishes them all.
+  template <class T, int K>
+  __device__ void reduce(T (&v)[K], T* scratch) {
+    if (spart == nullptr) {
+      block_sum<T, K>(v, scratch);
+      finish_sum<T, K>(v);
+      return;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] = warp_sum(v[i]);
+    double* p = sbuf();
+    if (lane < G) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) push(p + ((size_t)(r * nw + wid)) * K + i, lane, (double)v[i]);
+    }
+    sync();
+    const int tot = G * nw;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      T acc = T(0);
+      for (int e = lane; e < tot; e += 32) acc += (T)p[(size_t)e * K + i];
+      v[i] = warp_sum(acc);
+    }
+    ++phase;
   }
 
   // v[] holds this CTA's block-reduced values in every thread.
