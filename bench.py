@@ -50,6 +50,14 @@ def _rank_env():
         os.environ.get("LOCAL_RANK", "0"))
 
 
+def _tc_peak():
+    """dense fp16/bf16 tensor TFLOP/s (MEASURED_PEAKS.json burst; fallback 2250 nominal)"""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get("bf16_tflops", 2250.0)
+    return 2250.0
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -269,6 +277,64 @@ class BatchRun:
         return self.spec.batch * self.spec.n * 8
 
 
+KERNEL_CASES = [
+    # (name, n, (u_f, u, u_r), lu_modes): BASELINE configs[3] / configs[4] sizes
+    ("cfg4", 8192, ("single", "double", "quad"), ("exact",)),
+    ("cfg5", 16384, ("half", "single", "double"), ("exact", "tensor")),
+]
+
+
+def kernel_rooflines(torch, peak_gbs: float, peak_tf: float, reps: int = 10):
+    """Per-kernel evidence at the large configurations: the
+    preconditioned operator and the residual as standalone launches on
+    device-resident data (CUDA events, back-to-back launches, inputs larger
+    than L2), and the LU factorisation.  A: seeded N(0, 1/n) + 4 I generated
+    on the device (the operator/residual/LU cost does not depend on values)."""
+    from paper_2201_09827_b200 import _lib
+    from paper_2201_09827_b200.precision import PrecisionTriple
+    from paper_2201_09827_b200.refine import Method, RefineConfig, make_options
+
+    out = []
+    for name, n, prec, modes in KERNEL_CASES:
+        gen = torch.Generator(device="cuda").manual_seed(1)
+        a = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=gen) / math.sqrt(n)
+        a.diagonal().add_(4.0)
+        b = torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)
+        uf, u, ur = prec
+        bu, bf = _BYTES[u], _BYTES[uf]
+        for mode in modes:
+            cfg = RefineConfig(PrecisionTriple.parse(*prec), Method.RGMRES_IR, m=20, k=4, i_max=1, lu_mode=mode)
+            s = _lib.Solver(n, make_options(cfg, n))
+            s.set_system_device(a.data_ptr(), b.data_ptr())
+            s.factorize()
+            lu_ms = s.last_factor_ms
+            row = {"case": name, "n": n, "precisions": "/".join(prec), "lu_mode": mode,
+                   "lu_ms": lu_ms, "lu_tflops": 2.0 * n ** 3 / 3.0 / (lu_ms * 1e-3) / 1e12,
+                   "lu_frac_of_tc_peak": 2.0 * n ** 3 / 3.0 / (lu_ms * 1e-3) / 1e12 / peak_tf}
+            if mode == "exact":
+                v = np.random.default_rng(0).standard_normal(n)
+                s.apply_preconditioned(v, _FMT[_SQUARED[u]])
+                t_op = s.time_op(0, reps)
+                s.residual(v, _FMT[ur])
+                t_res = s.time_op(2, reps)
+                op_b = n * n * (bu + bf)
+                res_b = n * n * bu
+                row.update({"op_ms": t_op, "op_alg_bytes": op_b, "op_gbs": op_b / (t_op * 1e-3) / 1e9,
+                            "op_frac": op_b / (t_op * 1e-3) / 1e9 / peak_gbs,
+                            "residual_ms": t_res, "residual_alg_bytes": res_b,
+                            "residual_gbs": res_b / (t_res * 1e-3) / 1e9,
+                            "residual_frac": res_b / (t_res * 1e-3) / 1e9 / peak_gbs})
+            out.append(row)
+            del s
+        del a, b
+        torch.cuda.empty_cache()
+    return out
+
+
+_FMT = {"half": 0, "single": 1, "double": 2, "quad": 3}
+_SQUARED = {"half": "single", "single": "double", "double": "quad"}
+
+
 def _flush_l2(torch, buf):
     buf.add_(1.0)  # 512 MiB write > 126 MB L2
 
@@ -378,6 +444,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel cfg4/cfg5 rooflines")
     args = ap.parse_args()
     rank, world, local = _rank_env()
     specs = [_spec(s) for s in WORKLOADS[args.workload]]
@@ -504,6 +571,11 @@ def main():
                 hint[r.spec.name] = sum(r.last_report["inner_iters"]) or 1
         cpu = cpu_sample(args.workload, iters_hint=hint or _GOLDEN_ITERS)
     reports = [r.last_report for r in runs]
+    kernels = None
+    if not args.no_kernels and world == 1:
+        del runs
+        torch.cuda.empty_cache()
+        kernels = kernel_rooflines(torch, peak, _tc_peak())
     line = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -514,6 +586,7 @@ def main():
                    "time_to_solution_ms": total_ms / args.steps / len(specs) if specs[0].batch == 1 else None,
                    "verdicts": reports},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": int(launches),
+        "kernels": kernels,
     }
     print(json.dumps(line))
     if dist:

@@ -119,6 +119,12 @@ gb_status gb_precond_rhs(gb_solver* s, const double* r, double* out, int fmt);
 gb_status gb_residual(gb_solver* s, const double* x, double* r, int fmt);
 gb_status gb_lu_solve(gb_solver* s, const double* b, double* x);
 
+/* measurement: device time (ms) of one kernel-level launch of `what`
+ * (0 apply_preconditioned, 1 precond_rhs, 2 residual in u_r, 3 lu_solve),
+ * averaged over `reps` back-to-back launches on device-resident data (the
+ * vector of the last kernel-level call).  No reference counterpart. */
+gb_status gb_time_op(gb_solver* s, int what, int reps, double* ms_per_launch);
+
 /* diagnostics: arm a phase-timer log of `cap` (tag, globaltimer ns) entries
  * for subsequent launches; with out != NULL first copy the current log
  * (1 + 2*cap words: count, then pairs) out.  cap = 0 disarms. */

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgcrodr_b200.so")
+# GB_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("GB_LIB_PATH") or os.path.join(HERE, "libgcrodr_b200.so")
 
 # formats / methods (gcrodr_b200.h)
 HALF, SINGLE, DOUBLE, QUAD = 0, 1, 2, 3
@@ -27,7 +28,7 @@ EXPORTS = [
     "gb_set_system", "gb_set_system_device", "gb_launch_count", "gb_factorize", "gb_initial_solution", "gb_reference_solution",
     "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
-    "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog",
+    "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog", "gb_time_op",
 ]
 
 
@@ -100,12 +101,15 @@ def load(path: str | None = None):
         "gb_lu_solve": (C.c_int, [vp, vp, vp]),
         "gb_last_step_ms": (C.c_double, [vp]),
         "gb_debug_phaselog": (C.c_int, [vp, C.c_int, vp]),
+        "gb_time_op": (C.c_int, [vp, C.c_int, C.c_int, dp]),
         "gb_last_factor_ms": (C.c_double, [vp]),
         "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
                                        vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
     }
     for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:  # an older build under GB_LIB_PATH (A/B runs)
+            continue
         fn.restype = res
         fn.argtypes = args
     _LIB = lib
@@ -240,6 +244,13 @@ class Solver:
 
     def lu_solve(self, b) -> np.ndarray:
         return self._vec_op(self.lib.gb_lu_solve, b)
+
+    def time_op(self, what: int, reps: int = 10) -> float:
+        """Device ms of one kernel-level launch (0 apply, 1 precond_rhs,
+        2 residual, 3 lu_solve) on the vector of the last kernel-level call."""
+        ms = C.c_double()
+        _check(self.lib.gb_time_op(self.h, what, reps, C.byref(ms)), "gb_time_op")
+        return ms.value
 
     def phaselog(self, cap: int = 0, read: bool = True):
         """Diagnostics: read the current phase log (tag, ns) and re-arm with cap."""

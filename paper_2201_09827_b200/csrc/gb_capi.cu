@@ -197,6 +197,12 @@ gb_status gb_lu_solve(gb_solver* s, const double* b, double* x) {
   return s->ops->debug(s, b, x, 3, s->o.uf);
 }
 
+gb_status gb_time_op(gb_solver* s, int what, int reps, double* ms_per_launch) {
+  if (!s || !ms_per_launch || what < 0 || what > 3 || reps < 1) return fail(GB_ERR_ARG, "bad arguments");
+  if (!s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
+  return s->ops->time_op(s, what, reps, ms_per_launch);
+}
+
 gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out) {
   if (!s) return fail(GB_ERR_ARG, "null solver");
   if (out != nullptr && s->plog != nullptr) {

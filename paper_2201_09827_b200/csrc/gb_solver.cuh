@@ -807,6 +807,7 @@ struct VariantOps {
   gb_status (*debug)(gb_solver*, const double*, double*, int what, int fmt);
   gb_status (*get_x)(gb_solver*, double*);
   gb_status (*get_lu)(gb_solver*, double*, long long*);
+  gb_status (*time_op)(gb_solver*, int what, int reps, double* ms);
   gb_status (*batched)(int, int, const gb_options*, int, double, const double*, const double*, int, gb_batch_out*,
                        double*, cudaStream_t);
 };
@@ -1272,6 +1273,32 @@ struct Impl {
     return GB_OK;
   }
 
+  // device time of one kernel-level op launch (what as in debug(), operator
+  // in this solver's matvec format), averaged over `reps` back-to-back
+  // launches on device-resident data (the vector left in rtmp)
+  static gb_status time_op(gb_solver* s, int what, int reps, double* ms) {
+    P_t P = make(s);
+    if (what == 2) P.ur = s->o.ur == GB_QUAD ? UR_DD : (s->o.ur == GB_DOUBLE ? UR_F64 : UR_F32);
+    auto one = [&]() -> gb_status {
+      auto go = [&](auto kc, auto kg) { return s->G == 1 ? launch(s, kc, P, what) : launch(s, kg, P, what); };
+      if (what == 3) return go(k_debug<UM, TW, TF, MV, CtaTeam>, k_debug<UM, TW, TF, MV, GridTeam>);
+      return go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, GridTeam>);
+    };
+    gb_status e = one();  // warm-up
+    if (e != GB_OK) return e;
+    CK(cudaEventRecord(s->ev0, s->stream));
+    for (int i = 0; i < reps; ++i) {
+      e = one();
+      if (e != GB_OK) return e;
+    }
+    CK(cudaEventRecord(s->ev1, s->stream));
+    CK(cudaEventSynchronize(s->ev1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, s->ev0, s->ev1));
+    *ms = (double)t / reps;
+    return GB_OK;
+  }
+
   static gb_status get_x(gb_solver* s, double* x) {
     count_launch();
     k_to_f64<TW><<<64, 256, 0, s->stream>>>((const TW*)s->xs, s->n, s->dtmp);
@@ -1446,7 +1473,7 @@ struct Impl {
   }
 
   static const VariantOps* table() {
-    static const VariantOps t{setup, set_system, factor, x0, xref, step, debug, get_x, get_lu, batched};
+    static const VariantOps t{setup, set_system, factor, x0, xref, step, debug, get_x, get_lu, time_op, batched};
     return &t;
   }
 };
