@@ -26,6 +26,11 @@ namespace gb {
 // per-32-row-block record of the TRSV helpers: the dd inverse of the diagonal
 // block (1024 doubles) followed by the folded neighbour block (1024 doubles)
 constexpr int kInvStride = 2048;
+// row-block size of the grid-team substitution trsv_cta_g
+constexpr int kTrsvB = 64;
+// doubles per block record of B-row blocks: inverse (B^2) + folded neighbour (B^2)
+template <int B>
+__host__ __device__ constexpr int inv_stride() { return 2 * B * B; }
 
 // optional phase timers (globaltimer ns, CTA 0 thread 0); enabled per launch
 // by a non-null pointer.  slot 0 = count, then pairs (tag, t).

@@ -476,6 +476,108 @@ __global__ void k_diag_inv(const S* W, size_t ld, int n, double* lh, double* ll,
     diag_inv_block(W, ld, n, b, lh, ll, uh, ul);
 }
 
+// B-row versions of the two record builders above for the grid-team
+// substitution (trsv_cta_g): B threads per block, thread c builds column c;
+// record stride 2 B^2, inverse column-major then folded block row-major.
+template <int B, class S>
+__device__ void diag_inv_block_b(const S* W, size_t ld, int n, int b, double* lh, double* ll, double* uh,
+                               double* ul) {
+  constexpr int RS = inv_stride<B>();
+  const int c = threadIdx.x % B;
+  const int r0 = b * B;
+  const int m = min(B, n - r0);
+  dd x[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) x[i] = dd{0.0, 0.0};
+  if (c < m) {
+    x[c] = dd{1.0, 0.0};
+    for (int i = c + 1; i < m; ++i) {
+      dd s{0.0, 0.0};
+      for (int j = c; j < i; ++j) s = dd_add(s, dd_scale(to_d(W[(size_t)(r0 + i) * ld + r0 + j]), x[j]));
+      x[i] = dd_neg(s);
+    }
+  }
+  for (int i = 0; i < B; ++i) {
+    lh[(size_t)b * RS + c * B + i] = (i > c && c < m) ? x[i].hi : 0.0;
+    ll[(size_t)b * RS + c * B + i] = (i > c && c < m) ? x[i].lo : 0.0;
+    x[i] = dd{0.0, 0.0};
+  }
+  if (c < m) {
+    x[c] = dd_div(dd{1.0, 0.0}, dd{to_d(W[(size_t)(r0 + c) * ld + r0 + c]), 0.0});
+    for (int i = c - 1; i >= 0; --i) {
+      dd s{0.0, 0.0};
+      for (int j = i + 1; j <= c; ++j) s = dd_add(s, dd_scale(to_d(W[(size_t)(r0 + i) * ld + r0 + j]), x[j]));
+      const dd ri = dd_div(dd{1.0, 0.0}, dd{to_d(W[(size_t)(r0 + i) * ld + r0 + i]), 0.0});
+      x[i] = dd_neg(dd_mul(s, ri));
+    }
+  }
+  for (int i = 0; i < B; ++i) {
+    uh[(size_t)b * RS + c * B + i] = (i <= c && c < m) ? x[i].hi : 0.0;
+    ul[(size_t)b * RS + c * B + i] = (i <= c && c < m) ? x[i].lo : 0.0;
+  }
+}
+
+// Folded off-diagonal blocks (second half of each block record, row-major,
+// element (i, j) at b*2B^2 + B^2 + i*B + j):
+//   lower b >= 1:      D_b^-1 L_{b,b-1}   (D_b unit lower diagonal block)
+//   upper b <= nb - 2: U_bb^-1 U_{b,b+1}
+// so the block solve becomes y_b = D_b^-1 t' - M_b y_adjacent with t' free of
+// the adjacent block: only one B-term product waits on the neighbour.
+template <int B, class S>
+__device__ void diag_fold_block_b(const S* W, size_t ld, int n, int b, double* lh, double* ll, double* uh,
+                                double* ul) {
+  constexpr int RS = inv_stride<B>();
+  const int j = threadIdx.x % B;
+  const int nb = (n + B - 1) / B;
+  const int r0 = b * B;
+  const int m = min(B, n - r0);
+  double* fl_h = lh + (size_t)b * RS + B * B;
+  double* fl_l = ll + (size_t)b * RS + B * B;
+  double* fu_h = uh + (size_t)b * RS + B * B;
+  double* fu_l = ul + (size_t)b * RS + B * B;
+  const double* Li_h = lh + (size_t)b * RS;
+  const double* Li_l = ll + (size_t)b * RS;
+  const double* Ui_h = uh + (size_t)b * RS;
+  const double* Ui_l = ul + (size_t)b * RS;
+  for (int i = 0; i < B; ++i) {
+    dd sl{0.0, 0.0}, su{0.0, 0.0};
+    if (i < m) {
+      if (b >= 1) {
+        const int c = (b - 1) * B + j;
+        sl = dd{to_d(W[(size_t)(r0 + i) * ld + c]), 0.0};
+        for (int k = 0; k < i; ++k)
+          sl = dd_add(sl, dd_scale(to_d(W[(size_t)(r0 + k) * ld + c]), dd{Li_h[k * B + i], Li_l[k * B + i]}));
+      }
+      if (b + 1 < nb) {
+        const int c = (b + 1) * B + j;
+        if (c < n)
+          for (int k = i; k < m; ++k)
+            su = dd_add(su, dd_scale(to_d(W[(size_t)(r0 + k) * ld + c]), dd{Ui_h[k * B + i], Ui_l[k * B + i]}));
+      }
+    }
+    fl_h[i * B + j] = sl.hi;
+    fl_l[i * B + j] = sl.lo;
+    fu_h[i * B + j] = su.hi;
+    fu_l[i * B + j] = su.lo;
+  }
+}
+
+template <int B, class S>
+__global__ void k_diag_fold_b(const S* W, size_t ld, int n, double* lh, double* ll, double* uh, double* ul) {
+  const int bpc = blockDim.x / B;
+  const int nb = (n + B - 1) / B;
+  for (int b = blockIdx.x * bpc + (int)(threadIdx.x / B); b < nb; b += gridDim.x * bpc)
+    diag_fold_block_b<B>(W, ld, n, b, lh, ll, uh, ul);
+}
+
+template <int B, class S>
+__global__ void k_diag_inv_b(const S* W, size_t ld, int n, double* lh, double* ll, double* uh, double* ul) {
+  const int bpc = blockDim.x / B;
+  const int nb = (n + B - 1) / B;
+  for (int b = blockIdx.x * bpc + (int)(threadIdx.x / B); b < nb; b += gridDim.x * bpc)
+    diag_inv_block_b<B>(W, ld, n, b, lh, ll, uh, ul);
+}
+
 // max |U| over the upper triangle
 template <int M>
 __global__ void k_lu_umax(const typename LuT<M>::S* W, size_t ld, int n, LuStatus* st) {

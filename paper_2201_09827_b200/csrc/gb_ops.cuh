@@ -830,6 +830,183 @@ __device__ void trsv_cta(Team& t, int n, const TF* __restrict__ LU, size_t ldf, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Grid-team substitution with B-row blocks (B = kTrsvB = 64, n > 1024): the
+// same scheme as trsv_cta with larger blocks (half the links of the chain);
+// the block records are staged in shared memory while the far tiles are
+// accumulated.  Out of line so its registers do not burden k_step.
+// ---------------------------------------------------------------------------
+// xor-butterfly of compensated pairs over L lanes (L a power of two)
+template <int M, int L>
+GB_DEVICE CAcc<M> cbfly(CAcc<M> a) {
+#pragma unroll
+  for (int o = 1; o < L; o <<= 1) a.merge(a.xor_shfl(o));
+  return a;
+}
+
+// shared memory of trsv_cta<B>: tsh [2][B] T | ystage [8][B] T | block
+// record stage (D_b^-1 and M_b: 2 B^2 hi, + 2 B^2 lo in the dd mode)
+template <int M, int B>
+__host__ __device__ constexpr size_t trsv_cta_smem() {
+  return (2 + 8) * (size_t)B * sizeof(typename Arith<M>::T) + 2 * (size_t)B * (B + 1) * 8 * (M == MODE_DD ? 2 : 1);
+}
+
+template <int M, class Team, class TF, bool kLower, int B = kTrsvB>
+__device__ __noinline__ void trsv_cta_g(Team& t, int n, const TF* __restrict__ LU, size_t ldf, typename Arith<M>::T* y,
+                         const TrsvSync& ts, void* smem_raw, const double* __restrict__ inv_h,
+                         const double* __restrict__ inv_l) {
+  // Block b (B rows) is owned by CTA b mod G.  Lane layout: warp w owns rows
+  // RPW*w .. RPW*w+RPW-1 of the block; the LPR lanes of a row each cover CPL
+  // columns of every B-column tile, in runs of 4: column 4*LPR*g + 4*cg + e
+  // (vector loads from the factors, conflict-free shared-memory reads).  Every row sum is CPL MACs
+  // per lane (two compensated chains) plus a log2(LPR)-level butterfly, so
+  // the chain between blocks is: stage the neighbour's B entries, CPL MACs
+  // against the folded neighbour block M_b (staged in shared memory while
+  // the far tiles are accumulated), the butterfly and the push.
+  using Ar = Arith<M>;
+  using T = typename Ar::T;
+  constexpr int NW = 8;  // warps per CTA (blockDim 256)
+  constexpr int RPW = B / NW, LPR = 32 / RPW, CPL = B / LPR, YPL = B / 32;
+  constexpr int RS = inv_stride<B>();
+  static_assert(RPW * NW == B && LPR * RPW == 32 && CPL % 4 == 0, "unsupported TRSV block");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rq = lane / LPR, cg = lane % LPR;
+  constexpr int S = B + 1;  // padded row stride of the staged records
+  // column of this lane's j-th product (j = 4 g + e)
+  auto colj = [&](int j) { return (j >> 2) * 4 * LPR + 4 * cg + (j & 3); };
+  const int ri = wid * RPW + rq;  // row inside the block
+  const int nb = (n + B - 1) / B;
+  T* tsh = reinterpret_cast<T*>(smem_raw);        // [2][B]
+  T* ystage = tsh + 2 * B + wid * B;              // this warp's [B]
+  // staged record, row-major with stride S: D_b^-1 rows [0, B), M_b rows [B, 2B)
+  double* rst_h = reinterpret_cast<double*>(tsh + (2 + NW) * B);
+  double* rst_l = rst_h + 2 * B * S;  // dd mode only
+  uint4* yt = ts.ytag;
+  const unsigned tag = (unsigned)(2ull * ts.epoch + (kLower ? 1ull : 2ull));
+  const unsigned ftag = (unsigned)(2ull * ts.epoch + 1ull);
+  const int G = t.size();
+  // stage the B entries of tile column tc (warp-wide poll) into ystage
+  auto stage_tile = [&](int tc) {
+    __syncwarp();
+    // poll all YPL entries of this lane together (one round trip per poll)
+    T v[YPL];
+    bool ok[YPL];
+#pragma unroll
+    for (int h = 0; h < YPL; ++h) {
+      const int c = tc + h * 32 + lane;
+      v[h] = Ar::zero();
+      ok[h] = !(c < n) || ytag_get(yt, c, tag, v[h], ts.dsm);
+    }
+    for (;;) {
+      bool all = true;
+#pragma unroll
+      for (int h = 0; h < YPL; ++h) all = all && ok[h];
+      if (__all_sync(0xffffffffu, all)) break;
+#pragma unroll
+      for (int h = 0; h < YPL; ++h)
+        if (!ok[h]) ok[h] = ytag_get(yt, tc + h * 32 + lane, tag, v[h], ts.dsm);
+    }
+#pragma unroll
+    for (int h = 0; h < YPL; ++h) ystage[h * 32 + lane] = (tc + h * 32 + lane < n) ? v[h] : Ar::zero();
+    __syncwarp();
+  };
+  int it = 0;
+  for (int s = t.rank(); s < nb; s += G, ++it) {
+    const int b = kLower ? s : nb - 1 - s;
+    const int r = b * B + ri;
+    const bool rowok = r < n;
+    const int noff = kLower ? b : nb - 1 - b;
+    const int nfar = noff > 0 ? noff - 1 : 0;  // tiles before the adjacent block
+    const double* rec_h = inv_h + (size_t)b * RS;
+    const double* rec_l = inv_l + (size_t)b * RS;
+    __syncthreads();  // previous block's readers of the record stage are done
+    {
+      // stage D_b^-1 (and M_b when a neighbour exists): the loads overlap the
+      // far-tile accumulation; the chain then reads only shared memory
+      // D^-1 is column-major in the record: transpose into rows
+      for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
+        const int i = e % B, c = e / B;
+        rst_h[i * S + c] = __ldg(rec_h + e);
+        if constexpr (M == MODE_DD) rst_l[i * S + c] = __ldg(rec_l + e);
+      }
+      if (noff > 0)
+        for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
+          const int i = e / B, c = e % B;
+          rst_h[(B + i) * S + c] = __ldg(rec_h + B * B + e);
+          if constexpr (M == MODE_DD) rst_l[(B + i) * S + c] = __ldg(rec_l + B * B + e);
+        }
+    }
+    // own row's input: lower -> permuted right-hand side; upper -> forward result
+    T y0 = kLower ? (rowok ? Ar::ld(y + r) : Ar::zero()) : ytag_wait<M>(yt, r, rowok, ftag, ts.dsm);
+    CAcc<M> ca0, ca1;
+    double lv[CPL], ln[CPL];
+    const TF* lrow = LU + (size_t)(rowok ? r : 0) * ldf;
+    auto tile_col = [&](int q) { return (kLower ? q : nb - 1 - q) * B; };
+    auto load_row = [&](int tc, double (&d)[CPL]) {
+#pragma unroll
+      for (int g = 0; g < CPL / 4; ++g) {
+        double q4[4];
+        const int c = tc + colj(4 * g);
+        load4<TF>(lrow + c, c, n, rowok, q4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) d[4 * g + e] = q4[e];
+      }
+    };
+    if (nfar > 0) load_row(tile_col(0), lv);
+    for (int q = 0; q < nfar; ++q) {
+      const int tc = tile_col(q);
+      if (q + 1 < nfar) load_row(tile_col(q + 1), ln);
+      stage_tile(tc);
+#pragma unroll
+      for (int j = 0; j < CPL; j += 2) {
+        ca0.add(lv[j], ystage[colj(j)]);
+        ca1.add(lv[j + 1], ystage[colj(j + 1)]);
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) lv[j] = ln[j];
+    }
+    // t' = y0 - (far tiles) for this row (all LPR lanes of the row hold it)
+    T acc = Ar::zero();
+    if (nfar > 0) {
+      ca0.merge(ca1);
+      acc = T(cbfly<M, LPR>(ca0).get());
+    }
+    const T tp = Ar::sub(y0, acc);
+    T* tb = tsh + (it & 1) * B;
+    if (cg == 0) tb[ri] = tp;
+    __syncthreads();
+    // partial of D_b^-1 t' over this lane's columns (lower: unit diagonal
+    // implied), carried as a compensated pair through the chain below
+    CAcc<M> pa, pb;
+#pragma unroll
+    for (int j = 0; j < CPL; j += 2) {
+      const int e0 = ri * S + colj(j), e1 = ri * S + colj(j + 1);
+      pa.add_inv(rst_h[e0], M == MODE_DD ? rst_l[e0] : 0.0, tb[colj(j)]);
+      pb.add_inv(rst_h[e1], M == MODE_DD ? rst_l[e1] : 0.0, tb[colj(j + 1)]);
+    }
+    if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s] = gtimer();
+    // y_b = D_b^-1 t' - M_b y_adjacent
+    if (noff > 0) {
+      stage_tile((kLower ? b - 1 : b + 1) * B);
+      if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s + 2] = gtimer();
+#pragma unroll
+      for (int j = 0; j < CPL; j += 2) {
+        const int e0 = (B + ri) * S + colj(j), e1 = (B + ri) * S + colj(j + 1);
+        pa.add_inv(-rst_h[e0], M == MODE_DD ? -rst_l[e0] : 0.0, ystage[colj(j)]);
+        pb.add_inv(-rst_h[e1], M == MODE_DD ? -rst_l[e1] : 0.0, ystage[colj(j + 1)]);
+      }
+    }
+    pa.merge(pb);
+    T z = T(cbfly<M, LPR>(pa).get());
+    if (kLower) z = Ar::add(z, tp);
+    if (rowok) {
+      ytag_put(yt, r, z, tag, ts.dsm, cg, LPR);  // grid team: the cg == 0 lane stores
+      if (cg == 0) y[r] = z;
+    }
+    if (ts.stamps != nullptr && threadIdx.x == 0) ts.stamps[3 * s + 1] = gtimer();
+  }
+}
+
 template <int M, class TF>
 __host__ __device__ inline size_t trsv_smem_bytes(int nthreads) {
   return (size_t)(nthreads / 32) * 32 * 33 * sizeof(typename TileT<TF>::T) +
@@ -991,9 +1168,15 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
   bool done = false;
   if constexpr (Team::kGrid && Arith<M>::kInv) {
     if (s.linv_hi != nullptr && s.uinv_hi != nullptr && ts.ytag != nullptr) {
-      trsv_cta<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.linv_hi, s.linv_lo);
-      mark(ts.log, 12);
-      trsv_cta<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.uinv_hi, s.uinv_lo);
+      if constexpr (Team::kTB == kTrsvB) {
+        trsv_cta_g<M, Team, TF, true, kTrsvB>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.linv_hi, s.linv_lo);
+        mark(ts.log, 12);
+        trsv_cta_g<M, Team, TF, false, kTrsvB>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.uinv_hi, s.uinv_lo);
+      } else {
+        trsv_cta<M, Team, TF, true>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.linv_hi, s.linv_lo);
+        mark(ts.log, 12);
+        trsv_cta<M, Team, TF, false>(t, n, s.LU, s.ldf, ybuf, ts, smem, s.uinv_hi, s.uinv_lo);
+      }
       done = true;
     }
   }

@@ -113,6 +113,15 @@ struct MakeTeam<GridTeam> {
                     gridDim.x > 1 && cluster_ncta() == gridDim.x};
   }
 };
+template <>
+struct MakeTeam<ClusterTeam> {
+  template <class P>
+  GB_DEVICE static ClusterTeam make(const P& p) {
+    ClusterTeam t;
+    static_cast<GridTeam&>(t) = MakeTeam<GridTeam>::make(p);
+    return t;
+  }
+};
 
 __host__ __device__ inline size_t sm_doubles(int m, int k) { return (size_t)5 * m + 2 * k + 512; }
 
@@ -918,7 +927,18 @@ struct Impl {
     const int fc = fast_cap(m, k);
     return sm_doubles(m, k) * sizeof(double) + std::max(ops_bytes<TW, TF, MV>(), (size_t)fc * sizeof(double));
   }
-  static size_t smem_bytes(gb_solver* s) { return smem_bytes_for(s->o.m, s->o.k); }
+  // grid teams with kTrsvB-row blocks also stage a block record in the op
+  // region (trsv_cta_g); one-CTA and cluster teams keep the 32-row scheme
+  static int trsv_block(const gb_solver* s) { return (s->G > 1 && !s->cluster) ? kTrsvB : 32; }
+  static size_t smem_bytes(gb_solver* s) {
+    size_t b = smem_bytes_for(s->o.m, s->o.k);
+    if (trsv_block(s) == kTrsvB) {
+      const size_t need = sm_doubles(s->o.m, s->o.k) * sizeof(double) +
+                          std::max(trsv_cta_smem<MV, kTrsvB>(), trsv_cta_smem<MODE_F64, kTrsvB>());
+      b = std::max(b, need);
+    }
+    return b;
+  }
 
   // can G CTAs of this kernel (with `sm` bytes of smem each) run as one cluster?
   template <class KernT>
@@ -1002,7 +1022,8 @@ struct Impl {
       s->perm = a.take<int>(ldv);
       s->piv = a.take<int>(64);
       s->lust = a.take<LuStatus>(1);
-      const size_t ninv = (size_t)((n + 31) / 32) * kInvStride;
+      const size_t ninv = std::max((size_t)((n + 31) / 32) * kInvStride,
+                                   (size_t)((n + kTrsvB - 1) / kTrsvB) * inv_stride<kTrsvB>());
       s->linvh = a.take<double>(ninv);
       s->linvl = a.take<double>(ninv);
       s->uinvh = a.take<double>(ninv);
@@ -1117,10 +1138,20 @@ struct Impl {
     if (e != GB_OK) return e;
     count_launch(2);
     k_lu_rcp<S><<<std::max(1, std::min(1184, (s->n + 255) / 256)), 256, 0, s->stream>>>(W, s->lda, s->n, rh, rl);
-    const int nbk = (s->n + 31) / 32;
-    k_diag_inv<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
-    count_launch();
-    k_diag_fold<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
+    if (trsv_block(s) == kTrsvB) {
+      // grid teams: kTrsvB-row block records for trsv_cta_g
+      const int nbk = (s->n + kTrsvB - 1) / kTrsvB;
+      k_diag_inv_b<kTrsvB, S><<<std::max(1, (nbk + 1) / 2), 2 * kTrsvB, 0, s->stream>>>(W, s->lda, s->n, ilh, ill,
+                                                                                      iuh, iul);
+      count_launch();
+      k_diag_fold_b<kTrsvB, S><<<std::max(1, (nbk + 1) / 2), 2 * kTrsvB, 0, s->stream>>>(W, s->lda, s->n, ilh, ill,
+                                                                                       iuh, iul);
+    } else {
+      const int nbk = (s->n + 31) / 32;
+      k_diag_inv<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
+      count_launch();
+      k_diag_fold<S><<<std::max(1, (nbk + 3) / 4), 128, 0, s->stream>>>(W, s->lda, s->n, ilh, ill, iuh, iul);
+    }
     CK(cudaGetLastError());
     return GB_OK;
   }
@@ -1189,7 +1220,9 @@ struct Impl {
 
   static gb_status x0(gb_solver* s, int* reset) {
     P_t P = make(s);
-    gb_status e = s->G == 1 ? launch(s, k_x0<TW, TF, MV, CtaTeam>, P) : launch(s, k_x0<TW, TF, MV, GridTeam>, P);
+    gb_status e = s->G == 1   ? launch(s, k_x0<TW, TF, MV, CtaTeam>, P)
+                  : s->cluster ? launch(s, k_x0<TW, TF, MV, ClusterTeam>, P)
+                               : launch(s, k_x0<TW, TF, MV, GridTeam>, P);
     if (e != GB_OK) return e;
     int f = 0;
     CK(cudaMemcpyAsync(&f, s->flags, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
@@ -1221,7 +1254,8 @@ struct Impl {
       }
       P_t P = make(s);
       e = s->G == 1 ? launch(s, k_xref_refine<TW, TF, MV, CtaTeam>, P)
-                    : launch(s, k_xref_refine<TW, TF, MV, GridTeam>, P);
+                    : s->cluster ? launch(s, k_xref_refine<TW, TF, MV, ClusterTeam>, P)
+                                 : launch(s, k_xref_refine<TW, TF, MV, GridTeam>, P);
       if (e != GB_OK) return e;
     }
     int f = 0;
@@ -1234,7 +1268,9 @@ struct Impl {
   static gb_status step(gb_solver* s, gb_step_info* info) {
     P_t P = make(s);
     CK(cudaEventRecord(s->ev0, s->stream));
-    gb_status e = s->G == 1 ? launch(s, k_step<TW, TF, MV, CtaTeam>, P) : launch(s, k_step<TW, TF, MV, GridTeam>, P);
+    gb_status e = s->G == 1   ? launch(s, k_step<TW, TF, MV, CtaTeam>, P)
+                  : s->cluster ? launch(s, k_step<TW, TF, MV, ClusterTeam>, P)
+                               : launch(s, k_step<TW, TF, MV, GridTeam>, P);
     if (e != GB_OK) return e;
     CK(cudaEventRecord(s->ev1, s->stream));
     int kio[4];
@@ -1255,15 +1291,17 @@ struct Impl {
     CK(cudaMemcpyAsync(s->rtmp, in, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
     P_t P = make(s);
     gb_status e = GB_OK;
-    auto go = [&](auto kc, auto kg) { return s->G == 1 ? launch(s, kc, P, what) : launch(s, kg, P, what); };
+    auto go = [&](auto kc, auto kcl, auto kg) {
+      return s->G == 1 ? launch(s, kc, P, what) : s->cluster ? launch(s, kcl, P, what) : launch(s, kg, P, what);
+    };
     if (what == 2) {
       // residual(a, x, b, ctx): the mode template is irrelevant for it
       P.ur = fmt == GB_QUAD ? UR_DD : (fmt == GB_DOUBLE ? UR_F64 : UR_F32);
-      e = go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, GridTeam>);
+      e = go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, ClusterTeam>, k_debug<MV, TW, TF, MV, GridTeam>);
     } else if (what == 3) {
-      e = go(k_debug<UM, TW, TF, MV, CtaTeam>, k_debug<UM, TW, TF, MV, GridTeam>);
+      e = go(k_debug<UM, TW, TF, MV, CtaTeam>, k_debug<UM, TW, TF, MV, ClusterTeam>, k_debug<UM, TW, TF, MV, GridTeam>);
     } else if (fmt == op_format()) {
-      e = go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, GridTeam>);
+      e = go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, ClusterTeam>, k_debug<MV, TW, TF, MV, GridTeam>);
     } else {
       return fail(GB_ERR_UNSUPPORTED, "operator context differs from this solver's matvec format");
     }
@@ -1280,9 +1318,14 @@ struct Impl {
     P_t P = make(s);
     if (what == 2) P.ur = s->o.ur == GB_QUAD ? UR_DD : (s->o.ur == GB_DOUBLE ? UR_F64 : UR_F32);
     auto one = [&]() -> gb_status {
-      auto go = [&](auto kc, auto kg) { return s->G == 1 ? launch(s, kc, P, what) : launch(s, kg, P, what); };
-      if (what == 3) return go(k_debug<UM, TW, TF, MV, CtaTeam>, k_debug<UM, TW, TF, MV, GridTeam>);
-      return go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, GridTeam>);
+      auto go = [&](auto kc, auto kcl, auto kg) {
+        return s->G == 1 ? launch(s, kc, P, what) : s->cluster ? launch(s, kcl, P, what) : launch(s, kg, P, what);
+      };
+      if (what == 3)
+        return go(k_debug<UM, TW, TF, MV, CtaTeam>, k_debug<UM, TW, TF, MV, ClusterTeam>,
+                  k_debug<UM, TW, TF, MV, GridTeam>);
+      return go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, ClusterTeam>,
+                k_debug<MV, TW, TF, MV, GridTeam>);
     };
     gb_status e = one();  // warm-up
     if (e != GB_OK) return e;

@@ -37,6 +37,7 @@ GB_DEVICE void st_release(unsigned* p, unsigned v) {
 
 struct CtaTeam {
   static constexpr bool kGrid = false;
+  static constexpr int kTB = 32;
   GB_DEVICE int size() const { return 1; }
   GB_DEVICE int rank() const { return 0; }
   GB_DEVICE bool leader() const { return true; }
@@ -73,6 +74,7 @@ GB_DEVICE unsigned cluster_ncta() {
 
 struct GridTeam {
   static constexpr bool kGrid = true;
+  static constexpr int kTB = kTrsvB;  // substitution row block (trsv_cta_g)
   int G, r;
   GridCtl* ctl;
   double* partials;  // 2 buffers of G * kMaxK doubles
@@ -256,6 +258,14 @@ struct GridTeam {
     __syncthreads();
     ++phase;
   }
+};
+
+// A grid team of <= 16 CTAs launched as one thread-block cluster (the cfg2
+// size, n <= 1024): same protocol as GridTeam (sync() picks the cluster
+// barrier at run time), but its own type so its kernels use the 32-row
+// substitution and carry none of the 64-row code (register pressure).
+struct ClusterTeam : GridTeam {
+  static constexpr int kTB = 32;
 };
 
 }  // namespace gb
