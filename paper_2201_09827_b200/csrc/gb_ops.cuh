@@ -1027,13 +1027,12 @@ struct alignas(16) Vec16 {
 // One warp computes sum_j a[j] * v[j] (mode M) and optionally sum |a||v|.
 // 128-bit loads, kU independent accumulators per lane (memory-level
 // parallelism), deterministic combine and warp tree.
-template <int M, bool kAbs, class TA, class TV>
+template <int M, bool kAbs, class TA, class TV, int kU = 4>
 __device__ __forceinline__ typename Arith<M>::T row_dot_ex(const TA* __restrict__ arow, const TV* __restrict__ v,
                                                            int n, double* absdot) {
   using Ar = Arith<M>;
   using T = typename Ar::T;
   constexpr int VW = Vec16<TA>::N;
-  constexpr int kU = 4;
   const int lane = threadIdx.x & 31;
   if constexpr (M == MODE_DD) {
     // compensated (Dot2) accumulation: exact products, two_sum errors summed
@@ -1075,9 +1074,24 @@ __device__ __forceinline__ typename Arith<M>::T row_dot_ex(const TA* __restrict_
       ca[1].add(x, y);
       if (kAbs) ab[1] = __fma_rn(fabs(x), fabs(y), ab[1]);
     }
-    dd s = dd_add(dd_add(ca[0].get(), ca[1].get()), dd_add(ca[2].get(), ca[3].get()));
+    dd s;
+    if constexpr (kU == 4) {
+      s = dd_add(dd_add(ca[0].get(), ca[1].get()), dd_add(ca[2].get(), ca[3].get()));
+    } else {
+#pragma unroll
+      for (int h = kU / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int u = 0; u < h; ++u) ca[u].merge(ca[u + h]);
+      s = ca[0].get();
+    }
     s = warp_sum_dd(s);
-    if (kAbs) *absdot = warp_sum((ab[0] + ab[1]) + (ab[2] + ab[3]));
+    if (kAbs) {
+#pragma unroll
+      for (int h = kU / 2; h > 2; h >>= 1)
+#pragma unroll
+        for (int u = 0; u < h; ++u) ab[u] += ab[u + h];
+      *absdot = warp_sum((ab[0] + ab[1]) + (ab[2] + ab[3]));
+    }
     return s;
   }
   T acc[kU];
@@ -1121,6 +1135,13 @@ __device__ __forceinline__ typename Arith<M>::T row_dot_ex(const TA* __restrict_
     acc[1] = Ar::mac(acc[1], x, y);
     if (kAbs) ab[1] = __fma_rn(fabs(x), fabs(y), ab[1]);
   }
+#pragma unroll
+  for (int h = kU / 2; h > 2; h >>= 1)
+#pragma unroll
+    for (int u = 0; u < h; ++u) {
+      acc[u] = Ar::add(acc[u], acc[u + h]);
+      ab[u] += ab[u + h];
+    }
   T s = Ar::add(Ar::add(acc[0], acc[1]), Ar::add(acc[2], acc[3]));
   if constexpr (M == MODE_DD) {
     s = warp_sum_dd(s);
@@ -1156,7 +1177,10 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
     const int src = s.perm[i];
     typename Ar::T val;
     if (v != nullptr) {
-      val = row_dot<M>(s.A + (size_t)src * s.lda, v, n);
+      if constexpr (Team::kTB == kTrsvB)  // grid teams (n > 1024): rows stream from HBM, 8 x 16 B in flight per lane
+        val = row_dot_ex<M, false, TA, TV, 8>(s.A + (size_t)src * s.lda, v, n, nullptr);
+      else
+        val = row_dot<M>(s.A + (size_t)src * s.lda, v, n);
     } else {
       val = Ar::from(to_d(rvec[src]));
     }

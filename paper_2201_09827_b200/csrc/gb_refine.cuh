@@ -34,15 +34,17 @@ __device__ ResidOut residual_check(Team& t, const TA* A, size_t lda, int n, cons
     const TA* ar = A + (size_t)i * lda;
     double ca = 0.0;
     double ri;
+    // grid teams (n > 1024): long rows stream from HBM, 8 x 16 B in flight per lane
+    constexpr int kU = Team::kTB == kTrsvB ? 8 : 4;
     if (ur == UR_DD) {
-      dd acc = row_dot_ex<MODE_DD, true>(ar, x, n, &ca);
+      dd acc = row_dot_ex<MODE_DD, true, TA, TW, kU>(ar, x, n, &ca);
       dd rr = dd_add(dd{(double)b[i], 0.0}, dd_neg(acc));
       ri = dd_val(rr);
     } else if (ur == UR_F64) {
-      double acc = row_dot_ex<MODE_F64, true>(ar, x, n, &ca);
+      double acc = row_dot_ex<MODE_F64, true, TA, TW, kU>(ar, x, n, &ca);
       ri = __dsub_rn((double)b[i], acc);
     } else {
-      float acc = row_dot_ex<MODE_F32, true>(ar, x, n, &ca);
+      float acc = row_dot_ex<MODE_F32, true, TA, TW, kU>(ar, x, n, &ca);
       ri = (double)__fsub_rn((float)b[i], acc);
     }
     const double cd = ca + fabs((double)b[i]);
