@@ -94,10 +94,10 @@ static __device__ __noinline__ int blk_getrf(double* a, int ld, int p, int* piv)
     const double rp = 1.0 / pv;
     for (int i = k + 1 + threadIdx.x; i < p; i += blockDim.x) a[IX(i, k, ld)] *= rp;
     __syncthreads();
-    const int m = p - k - 1;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      int i = k + 1 + e % m, j = k + 1 + e / m;
-      a[IX(i, j, ld)] = __fma_rn(-a[IX(i, k, ld)], a[IX(k, j, ld)], a[IX(i, j, ld)]);
+    // trailing update: warp per column, lanes down the rows (no div/mod)
+    for (int j = k + 1 + wid; j < p; j += nw) {
+      const double akj = a[IX(k, j, ld)];
+      for (int i = k + 1 + lane; i < p; i += 32) a[IX(i, j, ld)] = __fma_rn(-a[IX(i, k, ld)], akj, a[IX(i, j, ld)]);
     }
     __syncthreads();
   }
@@ -122,13 +122,13 @@ static __device__ __noinline__ void blk_getrs(const double* a, int ld, int p, co
     }
   }
   __syncthreads();
-  // forward (unit lower)
+  // forward (unit lower); warp per right-hand side column, lanes down the rows
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = 0; j < p - 1; ++j) {
-    const int m = p - 1 - j;
-    for (int e = threadIdx.x; e < m * q; e += blockDim.x) {
-      const int i = j + 1 + e % m, c = e / m;
+    for (int c = wid; c < q; c += nw) {
       const double xj = b[IX(j, c, ldb)];
-      if (xj != 0.0) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
+      if (xj != 0.0)
+        for (int i = j + 1 + lane; i < p; i += 32) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
     }
     __syncthreads();
   }
@@ -138,10 +138,10 @@ static __device__ __noinline__ void blk_getrs(const double* a, int ld, int p, co
       if (b[IX(j, c, ldb)] != 0.0) b[IX(j, c, ldb)] = b[IX(j, c, ldb)] / a[IX(j, j, ld)];
     __syncthreads();
     if (j == 0) break;
-    for (int e = threadIdx.x; e < j * q; e += blockDim.x) {
-      const int i = e % j, c = e / j;
+    for (int c = wid; c < q; c += nw) {
       const double xj = b[IX(j, c, ldb)];
-      if (xj != 0.0) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
+      if (xj != 0.0)
+        for (int i = lane; i < j; i += 32) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
     }
     __syncthreads();
   }

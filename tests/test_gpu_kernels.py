@@ -168,3 +168,57 @@ def test_lu_tensor_core_mode(gpu):
     g = golden_json("cfg1")["rgmres-ir"]
     assert rep.converged and len(rep.inner_iters) == len(g["inner_iters"])
     assert all(abs(x - y) <= 2 for x, y in zip(rep.inner_iters, g["inner_iters"]))
+
+
+@pytest.mark.parametrize("u,u2", [("single", "double"), ("double", "quad")])
+def test_grid_team_operator(gpu, u, u2):
+    """n = 2048 runs as a cooperative grid team (G = 32 > 16) with the 64-row
+    substitution blocks (trsv_cta_g) and 8-deep GEMV loads: the operator,
+    precond_rhs and residual agree with the oracle applied to the SAME
+    factors (taken back from the device) to one rounding of u."""
+    rng = np.random.default_rng(11)
+    n = 2048
+    a = rng.standard_normal((n, n)) / np.sqrt(n) + 4.0 * np.eye(n)
+    b = rng.standard_normal(n)
+    s = _solver(a, b, "single", u)
+    zero, _ = s.factorize()
+    assert zero == -1
+    lu, perm = s.factors()
+    F = O.Factors(np.tril(lu, -1) + np.eye(n), np.triu(lu), perm.astype(np.int64), "single", 1.0)
+    a_u = O.rnd(a, u)
+    v = O.rnd(rng.standard_normal(n), u)
+    w = s.apply_preconditioned(v, _F[u2].code)
+    p = s.precond_rhs(v, _F[u2].code)
+    w_ref = O.apply_op(a_u, F, v, u2, u)
+    p_ref = O.precond_rhs(F, v, u2, u)
+    ulp = 2.0 ** -23 if u == "single" else 2.0 ** -52
+    for got, ref in ((w, w_ref), (p, p_ref)):
+        np.testing.assert_allclose(got, ref, rtol=ulp, atol=ulp * np.max(np.abs(ref)))
+    x = O.rnd(rng.standard_normal(n), u)
+    r = s.residual(x, Format.DOUBLE.code)
+    r_ref = O.residual(a_u, x, O.rnd(b, u), "double")
+    sc = np.max(np.abs(a_u)) * np.max(np.abs(x)) * n
+    np.testing.assert_allclose(r, r_ref, rtol=0, atol=4 * 2.0 ** -53 * sc)
+    s.close()
+
+
+def test_grid_team_solve(gpu):
+    """A full GCRO-DR-IR solve at n = 2048 (grid team) against the oracle:
+    same verdict, per-step iteration counts within +-1, same error levels."""
+    from paper_2201_09827_b200.refine import _refine
+
+    rng = np.random.default_rng(5)
+    n = 2048
+    q1, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    q2, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (q1 * np.geomspace(1.0, 1e-7, n)) @ q2.T
+    b = rng.standard_normal(n)
+    prec = ("single", "single", "double")  # oracle inner [10, 11]: cold + deflated cycles
+    cfg = RefineConfig(PrecisionTriple.parse(*prec), method=Method.RGMRES_IR, m=10, k=4, tau=1e-6, i_max=10)
+    rep = _refine(a, b, cfg)
+    ref = O.solve(a, b, prec, "rgmres-ir", 10, 4, 1e-6, 10)
+    assert rep.converged == ref.converged
+    assert len(rep.inner_iters) == len(ref.inner_iters)
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters, ref.inner_iters)
+    for got, want in ((rep.nbe_history[-1], ref.nbe_history[-1]), (rep.ferr_history[-1], ref.ferr_history[-1])):
+        assert got <= 10 * want + 2 * 2.0 ** -24, (got, want)

@@ -22,10 +22,10 @@ timeout 600 $NCU --set full --clock-control none --import-source on -k regex:k_d
   python tools/prof_kernels.py op 16384 half single double > $O/ncu_op16384.log 2>&1; summ ncu_op16384
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:k_debug -c 2 -o $O/ncu_op8192 -f \
   python tools/prof_kernels.py op 8192 single double quad > $O/ncu_op8192.log 2>&1; summ ncu_op8192
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_batched -c 1 -o $O/ncu_batched -f \
+  python tools/prof_kernels.py batched > $O/ncu_batched.log 2>&1; summ ncu_batched
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_lu_team -c 1 -o $O/ncu_lu_tensor -f \
   python tools/prof_kernels.py lu 16384 half single double tensor > $O/ncu_lu_tensor.log 2>&1; summ ncu_lu_tensor
 timeout 1200 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
   --log-file $O/launches_cfg2.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-kernels > $O/ncu_launches.log 2>&1
 du -sh $O
-cd tools/micro && timeout 300 $NCU --set full --import-source on -k k_hqr -c 2 -o ../../$O/hqr -f ./hqr > ../../$O/hqr_ncu.log 2>&1; cd ../..
-$NCU -i $O/hqr.ncu-rep --page source --csv --print-source cuda > $O/hqr_cuda_source.csv 2>&1; rm -f $O/hqr.ncu-rep

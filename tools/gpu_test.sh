@@ -1,7 +1,9 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
 PHASES=1 timeout 300 python tools/run_config.py cfg2a --imax 1 > $O/phases_cfg2a.log 2>&1
-timeout 1200 python bench.py > $O/bench_cfg2.log 2>&1; echo "rc $?" >> $O/bench_cfg2.log
-timeout 600 python bench.py --workload cfg3 --no-kernels > $O/bench_cfg3.log 2>&1; echo "rc $?" >> $O/bench_cfg3.log
+for i in 1 2; do
+timeout 300 python tools/prof_kernels.py op 8192 single double quad > $O/pk_op8192_$i.log 2>&1
+timeout 300 python tools/prof_kernels.py op 16384 half single double > $O/pk_op16384_$i.log 2>&1
+done
+timeout 600 python tools/run_config.py cfg4 > $O/run_cfg4.log 2>&1

@@ -2,6 +2,7 @@
   python tools/prof_kernels.py step N uf u ur m k cycles  -- one refinement step capped at `cycles` cycles
   python tools/prof_kernels.py lu N uf u ur mode          -- one factorisation (mode exact|tensor)
   python tools/prof_kernels.py op N uf u ur               -- one apply_preconditioned + one residual launch
+  python tools/prof_kernels.py batched                     -- one cfg3 batched launch (4096 x n=128)
 Prints the CUDA-event time of the launches."""
 import math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -11,7 +12,19 @@ from paper_2201_09827_b200 import _lib
 from paper_2201_09827_b200.precision import PrecisionTriple
 from paper_2201_09827_b200.refine import Method, RefineConfig, make_options
 
-what, n = sys.argv[1], int(sys.argv[2])
+what = sys.argv[1]
+if what == "batched":
+    import bench
+    from paper_2201_09827_b200.batched import solve_batched
+    spec = bench._spec("cfg3")
+    A, B = bench._inputs(spec, 0)
+    cfg = bench._cfg(spec)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    for _ in range(2):
+        r = solve_batched(None, None, cfg, on_device_ptrs=(Ad.data_ptr(), Bd.data_ptr()), count=spec.batch, n=spec.n)
+        print(f"batched ms {r.device_ms:.3f} converged {int(r.converged.sum())}")
+    sys.exit(0)
+n = int(sys.argv[2])
 uf, u, ur = sys.argv[3:6]
 gen = torch.Generator(device="cuda").manual_seed(0)
 a = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=gen) / math.sqrt(n)
