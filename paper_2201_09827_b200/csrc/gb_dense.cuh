@@ -183,15 +183,18 @@ static __device__ __noinline__ void blk_geqrf(double* a, int ld, int r, int c, d
       for (int i = j + 1 + threadIdx.x; i < r; i += blockDim.x) a[IX(i, j, ld)] *= scal;
     __syncthreads();
     if (threadIdx.x == 0) a[IX(j, j, ld)] = s_beta;
-    // apply H_j to columns j+1..c-1: one thread per column
-    if (tj != 0.0)
-      for (int l = j + 1 + threadIdx.x; l < c; l += blockDim.x) {
-        double wv = a[IX(j, l, ld)];
-        for (int i = j + 1; i < r; ++i) wv = __fma_rn(a[IX(i, j, ld)], a[IX(i, l, ld)], wv);
-        wv *= tj;
-        a[IX(j, l, ld)] -= wv;
-        for (int i = j + 1; i < r; ++i) a[IX(i, l, ld)] = __fma_rn(-wv, a[IX(i, j, ld)], a[IX(i, l, ld)]);
+    // apply H_j to columns j+1..c-1: one warp per column, lanes down the rows
+    if (tj != 0.0) {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int l = j + 1 + wid; l < c; l += nw) {
+        double wv = 0.0;
+        for (int i = j + 1 + lane; i < r; i += 32) wv = __fma_rn(a[IX(i, j, ld)], a[IX(i, l, ld)], wv);
+        wv = (warp_sum(wv) + a[IX(j, l, ld)]) * tj;
+        __syncwarp();
+        if (lane == 0) a[IX(j, l, ld)] -= wv;
+        for (int i = j + 1 + lane; i < r; i += 32) a[IX(i, l, ld)] = __fma_rn(-wv, a[IX(i, j, ld)], a[IX(i, l, ld)]);
       }
+    }
     __syncthreads();
   }
 }
@@ -264,12 +267,16 @@ static __device__ __noinline__ bool blk_qr_signed(double* a, int ld, int r, int 
 // y = R^-1 g for upper-triangular R (c x c, ld), zero-diagonal entries give 0
 // (the reference falls back to lstsq there; gmres.py:117-120).
 static __device__ __noinline__ void blk_upper_solve(const double* rmat, int ld, int c, const double* g, double* y) {
-  if (threadIdx.x == 0) {
+  // warp 0: lanes sum the solved part of row i, one warp reduction per row
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     for (int i = c - 1; i >= 0; --i) {
-      double s = g[i];
-      for (int j = i + 1; j < c; ++j) s = __fma_rn(-rmat[IX(i, j, ld)], y[j], s);
-      double d = rmat[IX(i, i, ld)];
-      y[i] = d != 0.0 ? s / d : 0.0;
+      double s = 0.0;
+      for (int j = i + 1 + lane; j < c; j += 32) s = __fma_rn(-rmat[IX(i, j, ld)], y[j], s);
+      s = warp_sum(s) + g[i];
+      const double d = rmat[IX(i, i, ld)];
+      if (lane == 0) y[i] = d != 0.0 ? s / d : 0.0;
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -283,15 +290,18 @@ static __device__ __noinline__ void blk_lstsq(double* g, int ld, int r, int c, c
   // tmp = Q^T rhs (apply reflectors in order)
   for (int i = threadIdx.x; i < r; i += blockDim.x) tmp[i] = rhs[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     for (int j = 0; j < c; ++j) {
-      double tj = tau[j];
+      const double tj = tau[j];
       if (tj == 0.0) continue;
-      double wv = tmp[j];
-      for (int i = j + 1; i < r; ++i) wv = __fma_rn(g[IX(i, j, ld)], tmp[i], wv);
-      wv *= tj;
-      tmp[j] -= wv;
-      for (int i = j + 1; i < r; ++i) tmp[i] = __fma_rn(-wv, g[IX(i, j, ld)], tmp[i]);
+      double wv = 0.0;
+      for (int i = j + 1 + lane; i < r; i += 32) wv = __fma_rn(g[IX(i, j, ld)], tmp[i], wv);
+      wv = (warp_sum(wv) + tmp[j]) * tj;
+      __syncwarp();
+      if (lane == 0) tmp[j] -= wv;
+      for (int i = j + 1 + lane; i < r; i += 32) tmp[i] = __fma_rn(-wv, g[IX(i, j, ld)], tmp[i]);
+      __syncwarp();
     }
   }
   __syncthreads();
