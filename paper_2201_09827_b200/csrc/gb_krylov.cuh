@@ -56,6 +56,7 @@ struct Krylov {
   // no substitution is running); nullptr -> global scratch only
   double* fast;
   int fast_cap;  // doubles
+  int ops_bytes;  // size of the shared op region (TRSV tiles / leader scratch)
 };
 
 // shared-memory need (doubles) of the leader's dense work at dimension p
@@ -862,7 +863,7 @@ GB_DEVICE double* gram_final(const Krylov<TW, TA, TF, MV>& K, const Team& t) {
 }
 
 template <class TW, class TA, class TF, int MV, class Team>
-__device__ void team_gram(Team& t, Krylov<TW, TA, TF, MV>& K, int keff, int j, double* sm) {
+__device__ void team_gram(Team& t, Krylov<TW, TA, TF, MV>& K, int keff, int j, double* sm, void* smem_ops) {
   using Acc = typename Fmt<TW>::Acc;
   const int gr = keff + j + 1, gc = keff + j, ldv = K.ldv;
   int lo, hi;
@@ -870,6 +871,32 @@ __device__ void team_gram(Team& t, Krylov<TW, TA, TF, MV>& K, int keff, int j, d
   double* part = Team::kGrid ? K.gram + (size_t)t.rank() * K.gram_stride : gram_final(K, t);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int total = gr * gc;
+  const int nr = hi - lo;
+  if ((size_t)nr * (gr + gc) * sizeof(TW) <= (size_t)K.ops_bytes) {
+    // stage this CTA's rows of W = [C, V] and Vh = [Ut, V] in shared memory
+    // (row-major, one coalesced pass), then every thread forms whole Gram
+    // entries from shared memory: no per-entry warp reduction on the path
+    TW* Ws = reinterpret_cast<TW*>(smem_ops);
+    TW* Vs = Ws + (size_t)nr * gr;
+    for (int c = wid; c < gr + gc; c += nw) {
+      const bool isw = c < gr;
+      const int cc = isw ? c : c - gr;
+      const int kk = keff;
+      const TW* col = isw ? (cc < kk ? K.C + (size_t)cc * ldv : K.V + (size_t)(cc - kk) * ldv)
+                          : (cc < kk ? K.Ut + (size_t)cc * ldv : K.V + (size_t)(cc - kk) * ldv);
+      TW* dst = isw ? Ws + cc : Vs + cc;
+      const int ld = isw ? gr : gc;
+      for (int r = lane; r < nr; r += 32) dst[(size_t)r * ld] = col[lo + r];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int a = e % gr, b = e / gr;
+      Acc acc = Acc(0);
+      for (int r = 0; r < nr; ++r) acc = Fmt<TW>::mac(acc, Ws[(size_t)r * gr + a], Vs[(size_t)r * gc + b]);
+      part[e] = (double)acc;
+    }
+    __syncthreads();
+  } else
   for (int e = wid; e < total; e += nw) {
     const int a = e % gr, b = e / gr;
     const TW* wa = a < keff ? K.C + (size_t)a * ldv : K.V + (size_t)(a - keff) * ldv;
@@ -1313,7 +1340,7 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
     mark(ts.log, 52);
     if (j >= 1) {
       // W^T Vh (gr x gc) in the work format: per-CTA partial Grams
-      team_gram(t, K, keff, j, sm);
+      team_gram(t, K, keff, j, sm, smem_ops);
       mark(ts.log, 53);
       if (t.leader()) {
         int kn = leader_recycle(t, K, keff, j, ts.log);

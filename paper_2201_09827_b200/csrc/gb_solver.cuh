@@ -541,6 +541,7 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
   K.keff_io = (int*)(base + Ly.keff_io);
   K.fast = fcap > 0 ? reinterpret_cast<double*>(ops) : nullptr;
   K.fast_cap = fcap;
+  K.ops_bytes = 0;  // batched mode: the op region holds the system (no staging)
   P.b = (const TW*)(base + Ly.b);
   P.xs = (TW*)(base + Ly.xs);
   P.r = (double*)(base + Ly.r);
@@ -879,6 +880,7 @@ struct Impl {
     K.keff_io = s->keff_io;
     K.fast = nullptr;
     K.fast_cap = fast_cap(s->o.m, s->o.k);
+    K.ops_bytes = (int)(smem_bytes(s) - sm_doubles(s->o.m, s->o.k) * sizeof(double));
     P.b = (const TW*)s->b;
     P.xs = (TW*)s->xs;
     P.r = s->r;

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/final2
+mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
+timeout 1200 python bench.py > $O/bench_cfg2.log 2>&1; echo "rc $?" >> $O/bench_cfg2.log
+timeout 600 python bench.py --workload cfg3 --no-kernels > $O/bench_cfg3.log 2>&1; echo "rc $?" >> $O/bench_cfg3.log
