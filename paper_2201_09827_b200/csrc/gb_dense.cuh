@@ -457,9 +457,99 @@ static __device__ __noinline__ double blk_cond2(double* b, int ld, int p, double
 // Schur form T; z (p x p) Schur vectors; wr, wi eigenvalues in Schur order.
 // Returns false on non-convergence.
 // ---------------------------------------------------------------------------
+// Schur-vector updates handed from the QR warp to a second warp (ring in
+// shared memory): type 0 = bulge reflector at column k (x, y, z, q, r),
+// type 1 = 2x2 standardisation rotation at (k-1, k) (p, q).  The QR warp's
+// dependent chain per bulge step no longer includes the Z update.
+struct ZRec {
+  double a[5];
+  int k, type, notlast;
+};
+constexpr int kZRing = 64;
+
 static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
                                 double* ort) {
+  // called by threads 0..63: warp 0 runs orthes + the QR iteration, warp 1
+  // applies the Schur-vector updates it pushes
+  __shared__ ZRec zring[kZRing];
+  __shared__ volatile int s_head, s_tail, s_done;
   const int lane = threadIdx.x & 31;
+  const int low_ = 0, high_ = p - 1;
+  if ((threadIdx.x >> 5) == 1) {
+    asm volatile("bar.sync 1, 64;" ::: "memory");  // Z initialised, ring reset
+    int tail = 0;
+    for (;;) {
+      const int head = s_head;
+      if (tail == head) {
+        if (s_done && tail == s_head) break;
+        continue;
+      }
+      __threadfence_block();
+      const volatile ZRec& R = zring[tail % kZRing];
+      const int k = R.k, type = R.type, nl = R.notlast;
+      const double a0 = R.a[0], a1 = R.a[1], a2 = R.a[2], a3 = R.a[3], a4 = R.a[4];
+      __syncwarp();
+      if (type == 0) {
+        for (int i = low_ + lane; i <= high_; i += 32) {
+          double pp = a0 * Z[IX(i, k, ldz)] + a1 * Z[IX(i, k + 1, ldz)];
+          if (nl) {
+            pp = pp + a2 * Z[IX(i, k + 2, ldz)];
+            Z[IX(i, k + 2, ldz)] = Z[IX(i, k + 2, ldz)] - pp * a4;
+          }
+          Z[IX(i, k, ldz)] = Z[IX(i, k, ldz)] - pp;
+          Z[IX(i, k + 1, ldz)] = Z[IX(i, k + 1, ldz)] - pp * a3;
+        }
+      } else {
+        for (int i = low_ + lane; i <= high_; i += 32) {
+          double zz = Z[IX(i, k - 1, ldz)];
+          Z[IX(i, k - 1, ldz)] = a3 * zz + a0 * Z[IX(i, k, ldz)];
+          Z[IX(i, k, ldz)] = a3 * Z[IX(i, k, ldz)] - a0 * zz;
+        }
+      }
+      __syncwarp();
+      ++tail;
+      if (lane == 0) s_tail = tail;
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    return true;
+  }
+  // producer side: lane 0 appends records and publishes the head every
+  // kZPub records (one fence per batch); ring space is re-checked only when
+  // the cached tail says the ring may be full
+  constexpr int kZPub = 8;
+  int zh = 0, zt = 0;  // lane 0's local head and cached tail
+  auto zpublish = [&]() {
+    __threadfence_block();
+    s_head = zh;
+  };
+  auto zpush = [&](int type, int k, int nl, double a0, double a1, double a2, double a3, double a4) {
+    if (lane == 0) {
+      if (zh - zt >= kZRing) {
+        zpublish();
+        while (zh - (zt = s_tail) >= kZRing) {
+        }
+      }
+      ZRec& R = zring[zh % kZRing];
+      R.a[0] = a0;
+      R.a[1] = a1;
+      R.a[2] = a2;
+      R.a[3] = a3;
+      R.a[4] = a4;
+      R.k = k;
+      R.type = type;
+      R.notlast = nl;
+      ++zh;
+      if (zh % kZPub == 0) zpublish();
+    }
+  };
+  auto zfinish = [&]() {
+    if (lane == 0) {
+      zpublish();
+      __threadfence_block();
+      s_done = 1;
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");  // the Z warp drained the ring
+  };
   const int nn = p, low = 0, high = p - 1;
   // --- orthes: Householder reduction to Hessenberg form ---
   for (int m = low + 1; m <= high - 1; ++m) {
@@ -522,7 +612,13 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
     int i = e % nn, j = e / nn;
     if (i > j + 1) H[IX(i, j, ld)] = 0.0;
   }
+  if (lane == 0) {
+    s_head = 0;
+    s_tail = 0;
+    s_done = 0;
+  }
   __syncwarp();
+  asm volatile("bar.sync 1, 64;" ::: "memory");  // start the Z warp
 
   // --- hqr2: Francis double-shift QR with accumulation ---
   int n = nn - 1;
@@ -595,11 +691,7 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           H[IX(i, n - 1, ld)] = q * zz + p_ * H[IX(i, n, ld)];
           H[IX(i, n, ld)] = q * H[IX(i, n, ld)] - p_ * zz;
         }
-        for (int i = low + lane; i <= high; i += 32) {
-          double zz = Z[IX(i, n - 1, ldz)];
-          Z[IX(i, n - 1, ldz)] = q * zz + p_ * Z[IX(i, n, ldz)];
-          Z[IX(i, n, ldz)] = q * Z[IX(i, n, ldz)] - p_ * zz;
-        }
+        zpush(1, n, 0, p_, 0.0, 0.0, q, 0.0);
         __syncwarp();
       } else {
         if (lane == 0) {
@@ -644,7 +736,10 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
         }
       }
       iter++;
-      if (++total > itmax) return false;
+      if (++total > itmax) {
+        zfinish();
+        return false;
+      }
       int m = n - 2;
       while (m >= l) {
         z = H[IX(m, m, ld)];
@@ -718,21 +813,14 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
             H[IX(i, k, ld)] = H[IX(i, k, ld)] - pp;
             H[IX(i, k + 1, ld)] = H[IX(i, k + 1, ld)] - pp * q;
           }
-          for (int i = low + lane; i <= high; i += 32) {
-            double pp = x * Z[IX(i, k, ldz)] + y * Z[IX(i, k + 1, ldz)];
-            if (notlast) {
-              pp = pp + z * Z[IX(i, k + 2, ldz)];
-              Z[IX(i, k + 2, ldz)] = Z[IX(i, k + 2, ldz)] - pp * r;
-            }
-            Z[IX(i, k, ldz)] = Z[IX(i, k, ldz)] - pp;
-            Z[IX(i, k + 1, ldz)] = Z[IX(i, k + 1, ldz)] - pp * q;
-          }
-          __syncwarp();
+          zpush(0, k, notlast ? 1 : 0, x, y, z, q, r);
+          __syncwarp();  // column update visible to the next step's scalars
         }
       }
     }
   }
   __syncwarp();
+  zfinish();
   return true;
 }
 

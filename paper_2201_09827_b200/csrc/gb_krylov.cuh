@@ -517,9 +517,9 @@ static __device__ __noinline__ int leader_ritz_basis(double* Mx, int p, int kreq
     if (!isfinite(Mx[e])) s_ok = 0;
   __syncthreads();
   if (!s_ok) return -1;
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < 64) {  // warp 0: QR iteration, warp 1: Schur-vector updates
     bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort);
-    if ((threadIdx.x & 31) == 0) s_ok = ok ? 1 : 0;
+    if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
   }
   __syncthreads();
   if (!s_ok) return -1;
