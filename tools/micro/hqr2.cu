@@ -1,6 +1,9 @@
 // A/B of the leader eigensolve (warp_hqr): the current gb_dense.cuh against
 // the previous version (old_dense.cuh, namespace gbold) -- bitwise-equal
 // Schur form, Schur vectors and eigenvalues, and cycles.
+//   old_dense.cuh = a previous gb_dense.cuh moved into namespace gbold:
+//     git show <rev>:paper_2201_09827_b200/csrc/gb_dense.cuh | sed 's/namespace gb {/namespace gbold {\nusing namespace gb;/;
+//       s/^}  \/\/ namespace gb/}  \/\/ namespace gbold/; s|#include "gb_common.cuh"|#include "../../paper_2201_09827_b200/csrc/gb_common.cuh"|' > old_dense.cuh
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a hqr2.cu -o hqr2
 #include <cstdio>
 #include <cstdlib>
