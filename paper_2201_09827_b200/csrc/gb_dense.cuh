@@ -122,27 +122,44 @@ static __device__ __noinline__ void blk_getrs(const double* a, int ld, int p, co
     }
   }
   __syncthreads();
-  // forward (unit lower); warp per right-hand side column, lanes down the rows
+  // forward (unit lower) and backward (upper) sweeps: lanes down the rows,
+  // each warp takes 4 right-hand-side columns per pass with all loads issued
+  // before the updates (the factor entry a(i, j) is loaded once per pass)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = 0; j < p - 1; ++j) {
-    for (int c = wid; c < q; c += nw) {
-      const double xj = b[IX(j, c, ldb)];
-      if (xj != 0.0)
-        for (int i = j + 1 + lane; i < p; i += 32) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
+  auto sweep = [&](int j, int i0, int i1) {
+    for (int c0 = wid; c0 < q; c0 += 4 * nw) {
+      double xj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * nw;
+        xj[u] = c < q ? b[IX(j, c, ldb)] : 0.0;
+      }
+      for (int i = i0 + lane; i < i1; i += 32) {
+        const double aij = a[IX(i, j, ld)];
+        double bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * nw;
+          bv[u] = c < q ? b[IX(i, c, ldb)] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * nw;
+          if (c < q && xj[u] != 0.0) b[IX(i, c, ldb)] = __fma_rn(-xj[u], aij, bv[u]);
+        }
+      }
     }
+  };
+  for (int j = 0; j < p - 1; ++j) {
+    sweep(j, j + 1, p);
     __syncthreads();
   }
-  // backward (upper)
   for (int j = p - 1; j >= 0; --j) {
     for (int c = threadIdx.x; c < q; c += blockDim.x)
       if (b[IX(j, c, ldb)] != 0.0) b[IX(j, c, ldb)] = b[IX(j, c, ldb)] / a[IX(j, j, ld)];
     __syncthreads();
     if (j == 0) break;
-    for (int c = wid; c < q; c += nw) {
-      const double xj = b[IX(j, c, ldb)];
-      if (xj != 0.0)
-        for (int i = lane; i < j; i += 32) b[IX(i, c, ldb)] = __fma_rn(-xj, a[IX(i, j, ld)], b[IX(i, c, ldb)]);
-    }
+    sweep(j, 0, j);
     __syncthreads();
   }
 }
