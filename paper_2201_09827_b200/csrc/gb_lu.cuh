@@ -700,27 +700,34 @@ __host__ __device__ inline size_t lu_team_smem(int n, int G) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, int i0, int j0, unsigned char* sA,
                                            unsigned char* sB, uint64_t* mbar, uint32_t tmem, uint32_t& phase) {
+  // Operands are staged with 16-byte shared-space stores (st.shared.v4 on
+  // the 32-bit shared address: the aligned staging pointer has lost its
+  // address space, so plain stores would be generic 2-byte ST.E).
+  const uint32_t sa = tc::smem_u32(sA), sb = tc::smem_u32(sB);
   // A: L21 rows [i0, i0+128), panel columns [k0, k0+32): K-major already
   for (int e = threadIdx.x; e < 128 * 4; e += blockDim.x) {
     const int r = e >> 2, c = e & 3;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     const int gi = i0 + r;
     if (gi < n) v = *reinterpret_cast<const uint4*>(W + (size_t)gi * ld + k0 + c * 8);
-    *reinterpret_cast<uint4*>(sA + tc::sw64_off(r, c * 8)) = v;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sa + tc::sw64_off(r, c * 8)), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
   }
-  // B: U12 rows [k0, k0+32), columns [j0, j0+256) transposed to K-major
-  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-    const int k = e >> 5, cj = e & 31;
-    const int gj = j0 + cj * 8;
+  // B: U12 rows [k0, k0+32), columns [j0, j0+256) transposed to K-major:
+  // item (column nn, k-chunk kc) gathers the 8 panel rows kc*8..kc*8+7 of one
+  // column (lanes take consecutive columns: coalesced 2-byte loads) into one
+  // 16-byte K-major store
+  for (int e = threadIdx.x; e < 256 * 4; e += blockDim.x) {
+    const int nn = e & 255, kc = e >> 8;
+    const int gj = j0 + nn;
     __align__(16) __half h[8];
-    if (gj + 8 <= n) {
-      *reinterpret_cast<uint4*>(h) = *reinterpret_cast<const uint4*>(W + (size_t)(k0 + k) * ld + gj);
-    } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) h[q] = (gj + q < n) ? W[(size_t)(k0 + k) * ld + gj + q] : __float2half(0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) *reinterpret_cast<__half*>(sB + tc::sw64_off(cj * 8 + q, k)) = h[q];
+    for (int q = 0; q < 8; ++q) h[q] = gj < n ? W[(size_t)(k0 + kc * 8 + q) * ld + gj] : __float2half(0.f);
+    const uint4 v = *reinterpret_cast<const uint4*>(h);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + tc::sw64_off(nn, kc * 8)), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
   }
   tc::fence_proxy_async();
   __syncthreads();
