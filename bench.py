@@ -132,7 +132,29 @@ def _cfg(spec, method="rgmres-ir"):
                         k=spec.k if method.startswith("r") else 0, tau=spec.tau, i_max=spec.i_max)
 
 
-def _inputs(spec, replica: int):
+def shard_systems(spec, rank: int, world: int) -> range:
+    """Multi-GPU decomposition.  Batched workloads (cfg3) are
+    weak-scaled shards: rank r solves systems r*batch .. (r+1)*batch - 1
+    (seeds 1 + index, disjoint across ranks, no data-path collective).  A
+    single-system workload does not shard: every rank solves the same system
+    as an independent replica."""
+    if spec.batch == 1:
+        return range(0, 1)
+    return range(rank * spec.batch, (rank + 1) * spec.batch)
+
+
+def max_over_ranks(value: float, dist, device) -> float:
+    """Whole-job time = the slowest rank's device time (the only collective)."""
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _inputs(spec, replica: int, world: int = 1):
     """Seeded inputs; replicas of single-system workloads perturb nothing (the
     configuration is one system) -- cfg3 shards draw systems seed+index."""
     from paper_2201_09827_b200 import problems
@@ -148,11 +170,11 @@ def _inputs(spec, replica: int):
         except OSError:
             pass
         return a, b
-    base = replica * spec.batch
+    idx = shard_systems(spec, replica, world)
     A = np.empty((spec.batch, spec.n, spec.n))
     B = np.empty((spec.batch, spec.n))
-    for i in range(spec.batch):
-        A[i], B[i] = problems.config_problem(spec, base + i)
+    for i, sysid in enumerate(idx):
+        A[i], B[i] = problems.config_problem(spec, sysid)
     return A, B
 
 
@@ -513,10 +535,7 @@ def main():
                     alg_bytes.extend(_alg_bytes(r.spec, [t]) for t in r.last_trace)
     launches = lib.gb_launch_count() - launches0
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, dist, "cuda")
     solves_per_step = sum(s.batch for s in specs)
     value = world * solves_per_step * args.steps / (total_ms / 1e3)
 

@@ -1,0 +1,68 @@
+"""World-size-2 `gloo` run of the multi-GPU decomposition on CPU:
+bench.py shards the batched workload (cfg3) into disjoint per-rank system
+ranges with no data-path collective, single-system workloads run as replicas,
+and the whole-job time is the max over ranks (the only collective)."""
+
+import dataclasses
+import hashlib
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, out):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from paper_2201_09827_b200 import problems
+
+        spec = dataclasses.replace(problems.CONFIGS["cfg3"], batch=3)
+        idx = list(bench.shard_systems(spec, rank, world))
+        a, b = bench._inputs(spec, rank, world)
+        digest = hashlib.sha256(a.tobytes() + b.tobytes()).hexdigest()
+        first_ok = bool(np.array_equal(a[0], problems.config_problem(spec, idx[0])[0]))
+        single = list(bench.shard_systems(problems.CONFIGS["cfg2a"], rank, world))
+        tmax = bench.max_over_ranks(1.5 + rank, dist, "cpu")
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (idx, digest, first_ok, single, tmax))
+        if rank == 0:
+            out.put(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharding_and_timing():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (i0, d0, ok0, s0, t0), (i1, d1, ok1, s1, t1) = res
+    # cfg3: disjoint, contiguous shards; each rank built its own systems
+    assert i0 == [0, 1, 2] and i1 == [3, 4, 5]
+    assert ok0 and ok1 and d0 != d1
+    # single-system workload: replicas of the same system
+    assert s0 == s1 == [0]
+    # the whole-job time is the slowest rank's
+    assert t0 == t1 == 2.5
