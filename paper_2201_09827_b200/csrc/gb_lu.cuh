@@ -658,6 +658,37 @@ __device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, i
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b] = acc[a][b] - s[a][b];
+  } else if constexpr (M == MODE_H16) {
+    // exact fp16 GEPP update fl16(a - fl16(l u)) on packed half2 pairs:
+    // __hmul2_rn / __hsub2_rn round each product and difference to fp16 and
+    // are never contracted into an fma, so every element sees the same
+    // operation sequence as the fp32-carried L::upd (double rounding through
+    // fp32 is innocuous: 24 >= 2*11 + 2) at a quarter of the instructions
+    __half2 acc2[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) acc2[a][p] = __floats2half2_rn(acc[a][2 * p], acc[a][2 * p + 1]);
+#pragma unroll 4
+    for (int k = 0; k < NB; ++k) {
+      __half2 l2[4], u2[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) l2[a] = __float2half2_rn(ls[(tr + 16 * a) * (NB + 1) + k]);
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+        u2[p] = __floats2half2_rn(us[k * (TN + 1) + tc + 16 * (2 * p)], us[k * (TN + 1) + tc + 16 * (2 * p + 1)]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) acc2[a][p] = __hsub2_rn(acc2[a][p], __hmul2_rn(l2[a], u2[p]));
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        acc[a][2 * p] = __low2float(acc2[a][p]);
+        acc[a][2 * p + 1] = __high2float(acc2[a][p]);
+      }
   } else {
 #pragma unroll 4
     for (int k = 0; k < NB; ++k) {
