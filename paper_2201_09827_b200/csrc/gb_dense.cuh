@@ -648,12 +648,22 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
   int iter = 0, total = 0;
   const int itmax = 40 * max(10, nn);
   while (n >= low) {
-    int l = n;
-    while (l > low) {
-      s = fabs(H[IX(l - 1, l - 1, ld)]) + fabs(H[IX(l, l, ld)]);
-      if (s == 0.0) s = norm;
-      if (fabs(H[IX(l, l - 1, ld)]) < eps * s) break;
-      l--;
+    // small-subdiagonal search (the first l from n downwards with a
+    // negligible H(l, l-1)), 32 candidates per ballot instead of a serial scan
+    int l = low;
+    for (int base = n; base > low; base -= 32) {
+      const int cand = base - lane;
+      bool hit = false;
+      if (cand > low) {
+        double sc = fabs(H[IX(cand - 1, cand - 1, ld)]) + fabs(H[IX(cand, cand, ld)]);
+        if (sc == 0.0) sc = norm;
+        hit = fabs(H[IX(cand, cand - 1, ld)]) < eps * sc;
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, hit);
+      if (bm) {
+        l = base - (__ffs(bm) - 1);
+        break;
+      }
     }
     if (l == n) {
       __syncwarp();
@@ -757,24 +767,43 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
         zfinish();
         return false;
       }
-      int m = n - 2;
-      while (m >= l) {
-        z = H[IX(m, m, ld)];
-        r = x - z;
-        s = y - z;
-        p_ = (r * s - w) / H[IX(m + 1, m, ld)] + H[IX(m, m + 1, ld)];
-        q = H[IX(m + 1, m + 1, ld)] - z - r - s;
-        r = H[IX(m + 2, m + 1, ld)];
-        s = fabs(p_) + fabs(q) + fabs(r);
-        p_ = p_ / s;
-        q = q / s;
-        r = r / s;
-        if (m == l) break;
-        if (fabs(H[IX(m, m - 1, ld)]) * (fabs(q) + fabs(r)) <
-            eps * (fabs(p_) * (fabs(H[IX(m - 1, m - 1, ld)]) + fabs(z) + fabs(H[IX(m + 1, m + 1, ld)]))))
+      // start of the double-shift sweep: the first m from n-2 downwards with
+      // two consecutive small subdiagonals (m = l always qualifies); 32
+      // candidates per ballot, then the chosen m's start vector is recomputed
+      // with exactly the operations of the serial EISPACK loop
+      int m = l;
+      for (int base = n - 2; base > l; base -= 32) {
+        const int mm = base - lane;
+        bool hit = false;
+        if (mm > l) {
+          const double zz = H[IX(mm, mm, ld)];
+          const double rr = x - zz, ss = y - zz;
+          double pp = (rr * ss - w) / H[IX(mm + 1, mm, ld)] + H[IX(mm, mm + 1, ld)];
+          double qq = H[IX(mm + 1, mm + 1, ld)] - zz - rr - ss;
+          double r3 = H[IX(mm + 2, mm + 1, ld)];
+          const double s3 = fabs(pp) + fabs(qq) + fabs(r3);
+          pp = pp / s3;
+          qq = qq / s3;
+          r3 = r3 / s3;
+          hit = fabs(H[IX(mm, mm - 1, ld)]) * (fabs(qq) + fabs(r3)) <
+                eps * (fabs(pp) * (fabs(H[IX(mm - 1, mm - 1, ld)]) + fabs(zz) + fabs(H[IX(mm + 1, mm + 1, ld)])));
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, hit);
+        if (bm) {
+          m = base - (__ffs(bm) - 1);
           break;
-        m--;
+        }
       }
+      z = H[IX(m, m, ld)];
+      r = x - z;
+      s = y - z;
+      p_ = (r * s - w) / H[IX(m + 1, m, ld)] + H[IX(m, m + 1, ld)];
+      q = H[IX(m + 1, m + 1, ld)] - z - r - s;
+      r = H[IX(m + 2, m + 1, ld)];
+      s = fabs(p_) + fabs(q) + fabs(r);
+      p_ = p_ / s;
+      q = q / s;
+      r = r / s;
       __syncwarp();
       for (int i = m + 2 + lane; i <= n; i += 32) {
         H[IX(i, i - 2, ld)] = 0.0;

@@ -24,7 +24,7 @@ __global__ void k_hqr(const double* A, int p, double* out, unsigned long long* c
   for (int e = threadIdx.x; e < p * p; e += blockDim.x) H[e] = A[e];
   __syncthreads();
   unsigned long long t0 = clock64();
-  if (threadIdx.x < (V == 0 ? 32 : 64)) {
+  if (threadIdx.x < 64) {
     bool r = V == 0 ? gbold::warp_hqr(H, p, p, Z, p, wr, wi, ort) : gb::warp_hqr(H, p, p, Z, p, wr, wi, ort);
     if (threadIdx.x == 0) *ok = r;
   }
