@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import enum
 import math
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -222,6 +223,43 @@ def _round_u(x: np.ndarray, u: Format) -> np.ndarray:
     return x
 
 
+# Device workspaces are kept between solves of the same order and options
+# (allocating and freeing ~n^2 buffers per call would dominate small solves).
+# A cached solver is taken out of the cache while in use, so concurrent calls
+# never share one; gb_set_system resets all per-solve device state.
+_SOLVER_CACHE: dict = {}
+_SOLVER_CACHE_MAX = 2
+_SOLVER_LOCK = threading.Lock()
+
+
+def _options_key(n: int, o) -> tuple:
+    return (n,) + tuple(getattr(o, f) for f, _ in o._fields_)
+
+
+def _acquire_solver(n: int, opts):
+    key = _options_key(n, opts)
+    with _SOLVER_LOCK:
+        cached = _SOLVER_CACHE.pop(key, None)
+    return key, (cached if cached is not None else _lib.Solver(n, opts))
+
+
+def _release_solver(key, solver) -> None:
+    with _SOLVER_LOCK:
+        if key not in _SOLVER_CACHE and len(_SOLVER_CACHE) < _SOLVER_CACHE_MAX:
+            _SOLVER_CACHE[key] = solver
+            return
+    solver.close()
+
+
+def release_workspaces() -> None:
+    """Free the device workspaces kept between solves."""
+    with _SOLVER_LOCK:
+        cached = list(_SOLVER_CACHE.values())
+        _SOLVER_CACHE.clear()
+    for s in cached:
+        s.close()
+
+
 def _refine(a, b, cfg: RefineConfig, *, trace: list | None = None, grid_ctas: int = 0) -> RefinementReport:
     prec = cfg.precisions
     if prec.u not in (Format.SINGLE, Format.DOUBLE):
@@ -239,11 +277,13 @@ def _refine(a, b, cfg: RefineConfig, *, trace: list | None = None, grid_ctas: in
         a, b, col_scale = _pow2_equilibrate(_round_u(a, prec.u), _round_u(b, prec.u))
         diagnostics["equilibrated"] = True
     opts = make_options(cfg, n, grid_ctas)
-    solver = _lib.Solver(n, opts)
+    key, solver = _acquire_solver(n, opts)
+    ok = False
     try:
         solver.set_system(a, b)
         zero, growth = solver.factorize()
         if zero >= 0:
+            ok = True
             return RefinementReport(False, 0, [], [], [], DivergenceReason.INNER_STAGNATION, None,
                                     {"lu_failed": f"exact zero pivot at column {zero}", **diagnostics})
         diagnostics["lu_growth"] = growth
@@ -285,10 +325,14 @@ def _refine(a, b, cfg: RefineConfig, *, trace: list | None = None, grid_ctas: in
         solution = solver.solution()
         if col_scale is not None:
             solution = col_scale * solution
+        ok = True
         return RefinementReport(converged, len(inner), inner, nbe_hist, ferr_hist,
                                 None if converged else reason, solution, diagnostics)
     finally:
-        solver.close()
+        if ok:
+            _release_solver(key, solver)
+        else:
+            solver.close()
 
 
 def sir(a, b, cfg: RefineConfig) -> RefinementReport:

@@ -2,5 +2,4 @@ cd $GRAFT_REPO_ROOT
 O=gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
-PHASES=1 timeout 300 python tools/run_config.py cfg2a --imax 1 > $O/phases_cfg2a.log 2>&1
 timeout 1200 python bench.py > $O/bench_cfg2.log 2>&1; echo "rc $?" >> $O/bench_cfg2.log
