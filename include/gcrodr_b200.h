@@ -58,6 +58,9 @@ typedef struct {
   int extra_precision;   /* operator at u^2 (1) or u (0) */
   int grid_ctas;         /* CTAs cooperating on one system; 0 = auto */
   int lu_mode;           /* 0 = exact (reference arithmetic) */
+  int explicit_residual; /* GmresConfig.restart_residual / GcrodrConfig.cycle_residual
+                           * != "recurrence": s - A~ x recomputed at each restart
+                           * (gmres.py:292-295, gcrodr.py:301-304, 376-379) */
 } gb_options;
 
 /* One refinement step (refine.py:362-407 loop body) */

@@ -45,7 +45,7 @@ class Options(C.Structure):
         ("uf", C.c_int), ("u", C.c_int), ("ur", C.c_int), ("method", C.c_int),
         ("m", C.c_int), ("k", C.c_int), ("tau", C.c_double), ("max_cycles", C.c_int),
         ("reorthogonalize", C.c_int), ("extra_precision", C.c_int), ("grid_ctas", C.c_int),
-        ("lu_mode", C.c_int),
+        ("lu_mode", C.c_int), ("explicit_residual", C.c_int),
     ]
 
 

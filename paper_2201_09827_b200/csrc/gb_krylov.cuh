@@ -34,6 +34,7 @@ struct Krylov {
   int n, ldv, m, k, max_cycles;
   double tau;
   int reorth, recycling;
+  int explicit_res;  // restart_residual / cycle_residual == "explicit"
   // problem
   SysView<TA, TF> sys;
   // long vectors (ldv stride)
@@ -489,6 +490,18 @@ __device__ void recurrence_res(Team& t, Krylov<TW, TA, TF, MV>& K, int steps, do
     for (int i = 0; i <= steps; ++i) acc = F::axpy(__ldcg(tv + i), K.V[(size_t)i * K.ldv + r], acc);
     K.res[r] = acc;
   }
+}
+
+// res = fl_u(s - A~ x): the explicit boundary residual (gmres.py:294-295,
+// gcrodr.py:301-304 and 376-379); one operator application, counted
+template <class TW, class TA, class TF, int MV, class Team>
+__device__ void explicit_residual(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& ts, void* smem_ops, int& applies) {
+  apply_A(t, K, ts, K.x, K.w, smem_ops, applies);
+  t.sync();
+  int lo, hi;
+  t.rows(K.n, lo, hi);
+  for (int r = lo + threadIdx.x; r < hi; r += blockDim.x) K.res[r] = K.s[r] - K.w[r];
+  t.sync();
 }
 
 // --------------------------------------------------------------------------
@@ -1164,7 +1177,10 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
       cycles++;
       breakdown = breakdown || co.breakdown;
       update_x(t, K.x, K.V, ldv, K.bc, j, n);
-      recurrence_res(t, K, j, beta);
+      if (co.converged || !K.explicit_res)
+        recurrence_res(t, K, j, beta);
+      else
+        explicit_residual(t, K, ts, smem_ops, applies);
       if (!K.recycling) {
         if (co.converged) {
           converged = true;
@@ -1337,6 +1353,7 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
       }
       K.res[r] = rr;
     }
+    if (K.explicit_res && !co.converged) explicit_residual(t, K, ts, smem_ops, applies);
     mark(ts.log, 52);
     if (j >= 1) {
       // W^T Vh (gr x gc) in the work format: per-CTA partial Grams

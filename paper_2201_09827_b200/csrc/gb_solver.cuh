@@ -472,7 +472,7 @@ struct BatchArgs {
   int *converged, *steps, *reason, *inner, *flags;
   double *nbe, *ferr, *x, *growth;
   // options
-  int m, k, max_cycles, reorth, method, ur, fast_cap;
+  int m, k, max_cycles, reorth, explicit_res, method, ur, fast_cap;
   double tau;
 };
 
@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(kThreads) k_batched(BatchArgs B) {
   K.max_cycles = B.max_cycles;
   K.tau = B.tau;
   K.reorth = B.reorth;
+  K.explicit_res = B.explicit_res;
   K.recycling = B.method == METH_GCRODR;
   TW* A = (TW*)(base + Ly.A);
   K.sys = SysView<TW, TF>{n,
@@ -846,6 +847,7 @@ struct Impl {
     K.max_cycles = s->o.max_cycles;
     K.tau = s->o.tau;
     K.reorth = s->o.reorthogonalize;
+    K.explicit_res = s->o.explicit_residual;
     K.recycling = (s->o.method == GB_RGMRES_IR || s->o.method == GB_RSGMRES_IR);
     K.sys = SysView<TW, TF>{s->n,     (size_t)s->lda, (const TW*)s->A, (size_t)s->lda, (const TF*)s->LU, s->perm,
                             s->rcph,  s->rcpl,        s->linvh,        s->linvl,        s->uinvh,          s->uinvl};
@@ -1484,6 +1486,7 @@ struct Impl {
     A.k = k;
     A.max_cycles = o->max_cycles;
     A.reorth = o->reorthogonalize;
+    A.explicit_res = o->explicit_residual;
     A.method = o->method == GB_SIR ? METH_SIR
                : (o->method == GB_GMRES_IR || o->method == GB_SGMRES_IR) ? METH_GMRES
                                                                           : METH_GCRODR;

@@ -186,8 +186,6 @@ def make_options(cfg: RefineConfig, n: int, grid_ctas: int = 0) -> _lib.Options:
         raise ValueError("recycling methods need 1 <= k < m")
     if not cfg.resolved_tau() > 0:
         raise ValueError("tolerance tau must be positive")
-    if cfg.restart_residual != "recurrence" or cfg.cycle_residual != "recurrence":
-        raise NotImplementedError("explicit restart/cycle residuals are not built (SURVEY §8(f) item 2)")
     o = _lib.Options()
     o.uf, o.u, o.ur = prec.uf.code, prec.u.code, prec.ur.code
     o.method = cfg.method.code
@@ -200,6 +198,11 @@ def make_options(cfg: RefineConfig, n: int, grid_ctas: int = 0) -> _lib.Options:
     if cfg.lu_mode not in ("exact", "tensor"):
         raise ValueError(f"unknown lu_mode {cfg.lu_mode!r}")
     o.lu_mode = 1 if cfg.lu_mode == "tensor" else 0
+    # any value other than "recurrence" recomputes s - A~ x at the restart,
+    # as the reference does (gmres.py:292-295; gcrodr.py:301-304, 376-379);
+    # plain GMRES reads restart_residual, GCRO-DR cycle_residual (refine.py:338, 352)
+    mode = cfg.cycle_residual if cfg.method.uses_recycling else cfg.restart_residual
+    o.explicit_residual = int(mode != "recurrence")
     return o
 
 

@@ -42,3 +42,29 @@ def test_no_gpu_means_loud_failure(monkeypatch):
         pytest.skip("a GPU is visible")
     with pytest.raises(_lib.GpuUnavailable):
         _lib.require_gpu()
+
+
+def test_options_block_matches_header():
+    """Every gb_options field in include/gcrodr_b200.h is in the ctypes mirror,
+    in the same order (the struct crosses the C-ABI by pointer)."""
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "gcrodr_b200.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} gb_options;", hdr, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = [n.strip() for decl in body.split(";") if decl.strip()
+             for n in decl.strip().split(None, 1)[1].split(",")]
+    assert names == [f[0] for f in _lib.Options._fields_]
+
+
+@pytest.mark.parametrize("method,restart,cycle,want", [
+    ("gmres-ir", "recurrence", "explicit", 0), ("gmres-ir", "explicit", "recurrence", 1),
+    ("rgmres-ir", "explicit", "recurrence", 0), ("rgmres-ir", "recurrence", "explicit", 1),
+    ("rsgmres-ir", "recurrence", "explicit", 1)])
+def test_residual_mode_option(method, restart, cycle, want):
+    """Plain GMRES reads restart_residual, GCRO-DR cycle_residual (refine.py:338, 352);
+    any value but "recurrence" means the explicit s - A~ x (gmres.py:292-295)."""
+    from paper_2201_09827_b200.precision import PrecisionTriple
+    from paper_2201_09827_b200.refine import Method, RefineConfig, make_options
+
+    cfg = RefineConfig(PrecisionTriple.parse("half", "single", "double"), Method.parse(method), m=8,
+                       k=3 if "r" == method[0] else 0, restart_residual=restart, cycle_residual=cycle)
+    assert make_options(cfg, 100).explicit_residual == want

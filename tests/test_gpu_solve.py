@@ -159,3 +159,47 @@ def test_config3_batched(gpu, method):
         check_report(rep, g[i], 2.0 ** -24, env=env)
         ref = np.array(g[i]["solution"])
         assert np.max(np.abs(rep.solution - ref)) <= 64 * 2.0 ** -24 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("mode", ["recurrence", "explicit"])
+@pytest.mark.parametrize("method,m,k", [("gmres-ir", 4, 0), ("rgmres-ir", 4, 2), ("gmres-ir", 8, 0),
+                                         ("rgmres-ir", 8, 3)])
+def test_restart_residual_modes(gpu, method, m, k, mode):
+    """restart_residual / cycle_residual = "explicit" (gmres.py:292-295,
+    gcrodr.py:301-304, 376-379): s - A~ x recomputed at each restart.  Config 1
+    with a short restart length so every step restarts; the oracle in the
+    same mode is the checker (verdict, per-step iterations +-1, error level,
+    solution to 4u)."""
+    from oracle import cpu_gcrodr_ir as O
+
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    prec = ("half", "single", "double")
+    cfg = RefineConfig(PrecisionTriple.parse(*prec), Method.parse(method), m=m, k=k, tau=1e-4, i_max=10,
+                       restart_residual=mode, cycle_residual=mode)
+    rep = _refine(a, b, cfg)
+    ref = O.solve(a, b, prec, method, m, k, 1e-4, 10, restart_residual=mode, cycle_residual=mode)
+    assert rep.converged == ref.converged
+    assert len(rep.inner_iters) == len(ref.inner_iters), (rep.inner_iters, ref.inner_iters)
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters, ref.inner_iters)
+    assert _level_ok(rep.nbe_history[-1], ref.nbe_history[-1], 10.0, 2.0 ** -24 * 0.05)
+    assert np.max(np.abs(rep.solution - ref.solution)) <= 4 * 2.0 ** -24 * np.max(np.abs(ref.solution))
+
+
+@pytest.mark.parametrize("mode", ["explicit"])
+def test_restart_residual_batched(gpu, mode):
+    """The batched kernel honours the same option (one CTA per system)."""
+    from oracle import cpu_gcrodr_ir as O
+    from paper_2201_09827_b200.batched import solve_batched
+
+    spec = problems.CONFIGS["cfg3"]
+    systems = [problems.config_problem(spec, i) for i in range(4)]
+    prec = ("half", "single", "double")
+    cfg = RefineConfig(PrecisionTriple.parse(*prec), Method.RGMRES_IR, m=6, k=2, tau=1e-4, i_max=10,
+                       cycle_residual=mode)
+    res = solve_batched(np.stack([s[0] for s in systems]), np.stack([s[1] for s in systems]), cfg)
+    for i, (a, b) in enumerate(systems):
+        rep = res.report(i)
+        ref = O.solve(a, b, prec, "rgmres-ir", 6, 2, 1e-4, 10, cycle_residual=mode)
+        assert rep.converged == ref.converged
+        assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters,
+                                                                                       ref.inner_iters)
