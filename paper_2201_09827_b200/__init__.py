@@ -7,7 +7,8 @@ The solver path is hand-written sm_100a CUDA behind a C ABI
 There is no CPU fallback.
 """
 
-from .precision import Format, PrecisionTriple, squared_format
+from .precision import (Format, PrecisionTriple, half_flushes_subnormals, set_half_flush_subnormals,
+                        squared_format)
 from .batched import solve_batched
 from .refine import (
     ConvergenceDecision,
@@ -28,6 +29,8 @@ __all__ = [
     "Format",
     "PrecisionTriple",
     "squared_format",
+    "set_half_flush_subnormals",
+    "half_flushes_subnormals",
     "Method",
     "DivergenceReason",
     "RefineConfig",

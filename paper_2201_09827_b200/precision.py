@@ -11,7 +11,15 @@ from dataclasses import dataclass
 
 from . import _lib
 
-__all__ = ["Format", "PrecisionTriple", "squared_format"]
+__all__ = ["Format", "PrecisionTriple", "squared_format", "set_half_flush_subnormals",
+           "half_flushes_subnormals"]
+
+# Process-wide half-precision subnormal handling (precision.py:111-128).  The
+# device kernels round fp16 with subnormals kept (the reference default);
+# solves that involve the half format refuse to run while flushing is on
+# (refine.make_options raises NotImplementedError) rather than silently
+# computing the non-flushed result.
+_HALF_FLUSH_TO_ZERO = False
 
 
 class Format(enum.Enum):
@@ -77,3 +85,17 @@ class PrecisionTriple:
     @classmethod
     def parse(cls, uf: str, u: str, ur: str) -> "PrecisionTriple":
         return cls(Format.parse(uf), Format.parse(u), Format.parse(ur))
+
+
+def set_half_flush_subnormals(enabled: bool) -> bool:
+    """Toggle flush-to-zero for the half format; returns the old setting
+    (precision.py:118-123)."""
+    global _HALF_FLUSH_TO_ZERO
+    old = _HALF_FLUSH_TO_ZERO
+    _HALF_FLUSH_TO_ZERO = bool(enabled)
+    return old
+
+
+def half_flushes_subnormals() -> bool:
+    """precision.py:126-127."""
+    return _HALF_FLUSH_TO_ZERO

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .precision import Format, PrecisionTriple, squared_format
+from .precision import Format, PrecisionTriple, half_flushes_subnormals, squared_format
 
 __all__ = [
     "Method",
@@ -186,6 +186,9 @@ def make_options(cfg: RefineConfig, n: int, grid_ctas: int = 0) -> _lib.Options:
         raise ValueError("recycling methods need 1 <= k < m")
     if not cfg.resolved_tau() > 0:
         raise ValueError("tolerance tau must be positive")
+    if half_flushes_subnormals() and Format.HALF in (prec.uf, prec.u, prec.ur):
+        raise NotImplementedError("half flush-to-zero (set_half_flush_subnormals(True)) is not built "
+                                  "on the device path")
     o = _lib.Options()
     o.uf, o.u, o.ur = prec.uf.code, prec.u.code, prec.ur.code
     o.method = cfg.method.code

@@ -68,3 +68,22 @@ def test_residual_mode_option(method, restart, cycle, want):
     cfg = RefineConfig(PrecisionTriple.parse("half", "single", "double"), Method.parse(method), m=8,
                        k=3 if "r" == method[0] else 0, restart_residual=restart, cycle_residual=cycle)
     assert make_options(cfg, 100).explicit_residual == want
+
+
+def test_half_flush_to_zero_refused_loudly():
+    """set_half_flush_subnormals (precision.py:118-127) is mirrored; the device
+    kernels keep fp16 subnormals, so half solves refuse to run while it is on."""
+    import paper_2201_09827_b200 as gb
+    from paper_2201_09827_b200.refine import make_options
+
+    cfg = gb.RefineConfig(gb.PrecisionTriple.parse("half", "single", "double"), gb.Method.RGMRES_IR, m=8, k=3)
+    assert gb.set_half_flush_subnormals(True) is False
+    try:
+        assert gb.half_flushes_subnormals()
+        with pytest.raises(NotImplementedError):
+            make_options(cfg, 100)
+        cfg2 = gb.RefineConfig(gb.PrecisionTriple.parse("single", "double", "double"), gb.Method.RGMRES_IR, m=8, k=3)
+        make_options(cfg2, 100)
+    finally:
+        assert gb.set_half_flush_subnormals(False) is True
+    make_options(cfg, 100)
