@@ -203,3 +203,28 @@ def test_restart_residual_batched(gpu, mode):
         assert rep.converged == ref.converged
         assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters,
                                                                                        ref.inner_iters)
+
+
+@pytest.mark.parametrize("prec", [("half", "single", "double"), ("single", "double", "double"),
+                                  ("half", "double", "double")])
+@pytest.mark.parametrize("method", ["sir", "sgmres-ir", "rsgmres-ir"])
+def test_sir_and_uniform_variants(gpu, method, prec):
+    """SIR (substitution only) and the uniform-precision S-variants (operator
+    at u instead of u^2; refine.py:56-83, 124-131, 378-380) on the config-1
+    system against the oracle in the same method: verdict and reason, per-step
+    iterations +-1, final nbe at the same level."""
+    from oracle import cpu_gcrodr_ir as O
+
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    m = 0 if method == "sir" else 100
+    k = 5 if method == "rsgmres-ir" else 0
+    tau = None if method == "sir" else 1e-4
+    cfg = RefineConfig(PrecisionTriple.parse(*prec), Method.parse(method), m=m, k=k, tau=tau, i_max=10)
+    rep = _refine(a, b, cfg)
+    ref = O.solve(a, b, prec, method, m, k, tau, 10)
+    u = {"single": 2.0 ** -24, "double": 2.0 ** -53}[prec[1]]
+    assert rep.converged == ref.converged
+    assert (rep.divergence_reason.value if rep.divergence_reason else None) == ref.divergence_reason
+    assert len(rep.inner_iters) == len(ref.inner_iters), (rep.inner_iters, ref.inner_iters)
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters, ref.inner_iters)
+    assert _level_ok(rep.nbe_history[-1], ref.nbe_history[-1], 10.0, u * 0.05), (rep.nbe_history, ref.nbe_history)
