@@ -1,0 +1,83 @@
+"""The sweep layer (reference harness.py:74-333) over the device solver."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_json
+from paper_2201_09827_b200 import harness
+from paper_2201_09827_b200.precision import PrecisionTriple
+from paper_2201_09827_b200.refine import Method, RefineConfig, RefinementReport
+
+
+def test_problem_ref_parse_and_ids():
+    p = harness.ProblemRef.parse("prolate:0.475")
+    assert (p.kind, p.alpha, p.n, p.problem_id) == ("prolate", 0.475, 100, "prolate:0.475")
+    r = harness.ProblemRef.parse("randsvd:1e12", n=64, seed=3)
+    assert (r.kappa2, r.n, r.seed, r.problem_id) == (1e12, 64, 3, "randsvd:1e+12")
+    assert harness.ProblemRef.parse("mtx:/data/bcsstk05.mtx").problem_id == "bcsstk05"
+    with pytest.raises(ValueError):
+        harness.ProblemRef.parse("toeplitz:3")
+
+
+def test_format_cell():
+    rep = RefinementReport(converged=True, steps=3, inner_iters=[10, 4, 4], nbe_history=[], ferr_history=[])
+    assert harness.format_cell(rep) == "18 (10,4,4)"
+    rep.converged = False
+    assert harness.format_cell(rep) == "-"
+
+
+def test_cond_inf_matches_definition():
+    a = harness.ProblemRef.parse("prolate:0.45", n=20).materialize()[0]
+    want = np.linalg.norm(a, np.inf) * np.linalg.norm(np.linalg.inv(a), np.inf)
+    assert math.isclose(harness.cond_inf(a), want, rel_tol=1e-12)
+
+
+def test_sweep_validation_and_in_row_errors():
+    spec = harness.SweepSpec([], [Method.GMRES_IR], PrecisionTriple.parse("single", "double", "quad"), m=16)
+    with pytest.raises(ValueError):
+        harness.run_sweep(spec)
+    spec = harness.SweepSpec([harness.ProblemRef.parse("mtx:/nonexistent.mtx")],
+                             [Method.GMRES_IR, Method.RGMRES_IR], PrecisionTriple.parse("single", "double", "quad"),
+                             m=16, k=4)
+    rows = harness.run_sweep(spec)
+    assert [r["method"] for r in rows] == ["gmres-ir", "rgmres-ir"]
+    assert [r["k"] for r in rows] == [0, 4]
+    assert all(r["divergence_reason"].startswith("error:") and r["cell"] == "-" for r in rows)
+    with pytest.raises(ValueError):
+        harness.kscan(harness.ProblemRef.parse("prolate:0.45"),
+                      RefineConfig(PrecisionTriple.parse("single", "double", "quad"), Method.RGMRES_IR, m=16, k=4),
+                      [4, 16])
+
+
+@pytest.mark.gpu
+def test_table5_sweep_on_device(gpu):
+    """Table 5 grid rows that are not chaotic (alpha >= 0.455) through run_sweep:
+    same verdict and per-step iterations +-1 against the reference's golden rows."""
+    rows = [r for r in golden_json("table5")["rows"] if r["alpha"] >= 0.455]
+    alphas = sorted({r["alpha"] for r in rows}, reverse=True)
+    spec = harness.SweepSpec([harness.ProblemRef.parse(f"prolate:{a}") for a in alphas],
+                             [Method.GMRES_IR, Method.RGMRES_IR], PrecisionTriple.parse("single", "double", "quad"),
+                             m=16, k=4, tau=1e-8)
+    got = harness.run_sweep(spec)
+    assert len(got) == 2 * len(alphas)
+    for g in got:
+        want = next(r for r in rows if f"prolate:{r['alpha']:g}" == g["problem_id"] and r["method"] == g["method"])
+        assert g["converged"] == want["converged"], g
+        per = [int(c) for c in g["per_step"].split(";")]
+        assert len(per) == len(want["inner_iters"]), (per, want["inner_iters"])
+        assert all(abs(x - y) <= 1 for x, y in zip(per, want["inner_iters"])), (per, want["inner_iters"])
+        assert g["kappa_inf"] > 1.0 and g["report"]["total_inner"] == sum(per)
+
+
+@pytest.mark.gpu
+def test_kscan_on_device(gpu):
+    """Recycle-dimension scan (Fig. 2 shape): one row per k, totals positive
+    for converged runs, -1 for divergent ones."""
+    cfg = RefineConfig(PrecisionTriple.parse("single", "double", "quad"), Method.RGMRES_IR, m=16, k=4, tau=1e-8)
+    rows = harness.kscan(harness.ProblemRef.parse("prolate:0.455"), cfg, [1, 2, 4, 8])
+    assert [r["k"] for r in rows] == [1, 2, 4, 8]
+    assert all(r["total_inner"] == -1 or r["total_inner"] > 0 for r in rows)
+    k4 = next(r for r in golden_json("table5")["rows"] if r["alpha"] == 0.455 and r["method"] == "rgmres-ir")
+    assert abs(rows[2]["total_inner"] - sum(k4["inner_iters"])) <= len(k4["inner_iters"])
