@@ -5,9 +5,7 @@ the recycle-dimension scan (Fig. 2).
 Every solve goes through ``refine.solve`` (the CUDA path).  The per-problem
 condition numbers in a row are problem statistics (numpy on the host, as the
 reference computes them: densela.py:491-503) and are not part of any timed
-solve.  Matrix Market problems are not built (``.mtx`` ingestion is SURVEY
-§8(f) item 4); such rows are recorded in-row as errors, as the reference
-records any per-problem failure.
+solve.  ``mtx:`` problems are read by ``mtx.read_matrix_market``.
 """
 
 from __future__ import annotations
@@ -18,6 +16,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import problems
+from .mtx import read_matrix_market
 from .precision import PrecisionTriple
 from .refine import Method, RefineConfig, RefinementReport, solve
 
@@ -54,7 +53,7 @@ class ProblemRef:
         elif self.kind == "randsvd":
             a = problems.randsvd(self.n, self.kappa2, self.seed)
         elif self.kind == "mtx":
-            raise NotImplementedError("Matrix Market ingestion is not built (SURVEY §8(f) item 4)")
+            a = read_matrix_market(self.path)
         else:
             raise ValueError(f"unknown problem kind {self.kind!r}")
         return a, problems.rhs_ones(a.shape[0])

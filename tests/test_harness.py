@@ -81,3 +81,67 @@ def test_kscan_on_device(gpu):
     assert all(r["total_inner"] == -1 or r["total_inner"] > 0 for r in rows)
     k4 = next(r for r in golden_json("table5")["rows"] if r["alpha"] == 0.455 and r["method"] == "rgmres-ir")
     assert abs(rows[2]["total_inner"] - sum(k4["inner_iters"])) <= len(k4["inner_iters"])
+
+
+def _write(tmp_path, name, text):
+    p = tmp_path / name
+    p.write_text(text)
+    return str(p)
+
+
+def test_mtx_coordinate_symmetric_and_duplicates(tmp_path):
+    from paper_2201_09827_b200.mtx import read_matrix_market
+
+    path = _write(tmp_path, "s.mtx", "%%MatrixMarket matrix coordinate real symmetric\n% c\n\n3 3 4\n"
+                  "1 1 2.0\n2 1 -1.5\n3 3 4\n2 1 0.5\n")
+    a = read_matrix_market(path)
+    assert np.array_equal(a, np.array([[2.0, -1.0, 0.0], [-1.0, 0.0, 0.0], [0.0, 0.0, 4.0]]))
+
+
+def test_mtx_array_layouts(tmp_path):
+    from paper_2201_09827_b200.mtx import read_matrix_market
+
+    gen = read_matrix_market(_write(tmp_path, "g.mtx", "%%MatrixMarket matrix array real general\n2 3\n"
+                                    "1\n2\n3\n4\n5\n6\n"))
+    assert np.array_equal(gen, np.array([[1.0, 3.0, 5.0], [2.0, 4.0, 6.0]]))
+    sym = read_matrix_market(_write(tmp_path, "y.mtx", "%%MatrixMarket matrix array integer symmetric\n3 3\n"
+                                    "1\n2\n3\n4\n5\n6\n"))
+    assert np.array_equal(sym, np.array([[1.0, 2.0, 3.0], [2.0, 4.0, 5.0], [3.0, 5.0, 6.0]]))
+
+
+@pytest.mark.parametrize("text,line,kind", [
+    ("", 1, "parse"),
+    ("%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n", None, "field"),
+    ("%%MatrixMarket matrix coordinate real skew-symmetric\n1 1 0\n", None, "field"),
+    ("%%MatrixMarket vector coordinate real general\n", 1, "parse"),
+    ("%%MatrixMarket matrix coordinate real general\n", 1, "parse"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2\n", 2, "parse"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n", 3, "parse"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 x\n", 3, "parse"),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n", 3, "parse"),
+    ("%%MatrixMarket matrix array real general\n2 2\n1\n2\n3\n", 5, "parse"),
+])
+def test_mtx_errors(tmp_path, text, line, kind):
+    from paper_2201_09827_b200.mtx import ParseError, UnsupportedField, read_matrix_market
+
+    path = _write(tmp_path, "e.mtx", text)
+    if kind == "field":
+        with pytest.raises(UnsupportedField):
+            read_matrix_market(path)
+    else:
+        with pytest.raises(ParseError) as exc:
+            read_matrix_market(path)
+        assert exc.value.line_no == line
+
+
+def test_mtx_round_trip_and_sweep_problem(tmp_path):
+    from paper_2201_09827_b200.mtx import read_matrix_market, write_matrix_market
+
+    a = harness.ProblemRef.parse("prolate:0.45", n=12).materialize()[0]
+    a[3, 5] = 0.0
+    path = str(tmp_path / "p45.mtx")
+    write_matrix_market(path, a, comment="prolate 0.45\nn = 12")
+    assert np.array_equal(read_matrix_market(path), a)
+    ref = harness.ProblemRef.parse(f"mtx:{path}")
+    got, b = ref.materialize()
+    assert ref.problem_id == "p45" and np.array_equal(got, a) and np.array_equal(b, np.ones(12))
