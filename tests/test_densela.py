@@ -43,7 +43,7 @@ def test_densela_mirror_matches_oracle(gpu, tag, uf, u):
     tol = 2.0 ** -23 if u == "single" else 2.0 ** -51
     for got, want in ((w, k[f"{tag}_op"]), (p, k[f"{tag}_prhs"])):
         np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.max(np.abs(want)))
-    rq = densela.residual(a, k[f"{tag}_x"], b, Format.QUAD)
+    rq = densela.residual(a, k[f"{tag}_x"], O.rnd(b, u), Format.QUAD)  # b held at u, as the solve does
     np.testing.assert_allclose(rq, k[f"{tag}_res_q"], rtol=0, atol=1e-30 + 2 ** -52 * np.max(np.abs(rq)))
     F.close()
 
