@@ -9,7 +9,7 @@ There is no CPU fallback.
 
 from .precision import (Format, PrecisionTriple, half_flushes_subnormals, set_half_flush_subnormals,
                         squared_format)
-from . import densela, harness, mtx
+from . import densela, mtx
 from .batched import solve_batched
 from .refine import (
     ConvergenceDecision,

@@ -10,17 +10,21 @@ solve.  ``mtx:`` problems are read by ``mtx.read_matrix_market``.
 
 from __future__ import annotations
 
+import argparse
+import json
 import math
+import sys
 from dataclasses import dataclass, replace
 
 import numpy as np
 
 from . import problems
-from .mtx import read_matrix_market
-from .precision import PrecisionTriple
+from .mtx import read_matrix_market, write_matrix_market
+from .precision import PrecisionTriple, set_half_flush_subnormals
 from .refine import Method, RefineConfig, RefinementReport, solve
 
-__all__ = ["ProblemRef", "SweepSpec", "format_cell", "run_sweep", "kscan", "cond_inf", "CSV_COLUMNS"]
+__all__ = ["ProblemRef", "SweepSpec", "format_cell", "run_sweep", "kscan", "cond_inf", "emit", "main",
+           "CSV_COLUMNS"]
 
 # harness.py:55-70
 CSV_COLUMNS = ["problem_id", "kappa_inf", "kappa_2", "method", "m", "k", "tau", "converged", "steps",
@@ -189,3 +193,158 @@ def kscan(problem: ProblemRef, cfg: RefineConfig, k_range) -> list:
         rep = solve(a, b, replace(cfg, k=int(k)))
         rows.append({"k": int(k), "total_inner": rep.total_inner if rep.converged else -1})
     return rows
+
+
+# ---------------------------------------------------------------------------
+# serialisation and the command line (harness.py:335-565)
+# ---------------------------------------------------------------------------
+
+def _cell_text(v) -> str:
+    if isinstance(v, bool):
+        return "true" if v else "false"
+    if isinstance(v, float):
+        return repr(v)
+    return str(v)
+
+
+def _md_table(columns: list, body: list) -> list:
+    return ["| " + " | ".join(columns) + " |", "|" + "|".join(" --- " for _ in columns) + "|"] + \
+           ["| " + " | ".join(cells) + " |" for cells in body]
+
+
+def emit(rows: list, fmt: str, path) -> None:
+    """Write sweep / kscan rows as csv, markdown or json, deterministically
+    (harness.py:343-381)."""
+    sweep_rows = not rows or "problem_id" in rows[0]
+    if fmt == "csv":
+        cols = CSV_COLUMNS if sweep_rows else list(rows[0])
+        text = [",".join(cols)] + [",".join(_cell_text(r.get(c, "")) for c in cols) for r in rows]
+    elif fmt == "markdown":
+        if rows and sweep_rows:
+            cols = ["problem_id", "method", "m", "k", "result", "converged", "nbe_final"]
+            body = [[str(r["problem_id"]), str(r["method"]), str(r["m"]), str(r["k"]), r.get("cell", "-"),
+                     _cell_text(r["converged"]), _cell_text(r["nbe_final"])] for r in rows]
+        else:
+            cols = list(rows[0]) if rows else []
+            body = [[_cell_text(r[c]) for c in cols] for r in rows]
+        text = _md_table(cols, body)
+    elif fmt == "json":
+        text = [json.dumps(rows, indent=2, allow_nan=True)]
+    else:
+        raise ValueError(f"unknown output format {fmt!r}")
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("\n".join(text) + "\n")
+
+
+def _parser() -> argparse.ArgumentParser:
+    ap = argparse.ArgumentParser(prog="paper_2201_09827_b200.harness",
+                                 description="Mixed-precision iterative refinement experiments on the GPU")
+    sub = ap.add_subparsers(dest="command", required=True)
+
+    def precision_flags(p):
+        p.add_argument("--uf", default="single")
+        p.add_argument("--u", default="double")
+        p.add_argument("--ur", default="quad")
+
+    def solver_flags(p):
+        p.add_argument("--m", type=int, default=40)
+        p.add_argument("--k", type=int, default=0)
+        p.add_argument("--tau", type=float, default=None)
+        p.add_argument("--imax", type=int, default=10000)
+        p.add_argument("--seed", type=int, default=1)
+        p.add_argument("--n", type=int, default=100)
+        p.add_argument("--scale-diag", action="store_true")
+        p.add_argument("--half-ftz", action="store_true")
+
+    p = sub.add_parser("solve")
+    p.add_argument("--problem", required=True)
+    p.add_argument("--method", default="gmres-ir")
+    precision_flags(p), solver_flags(p)
+    p.add_argument("--out", default=None)
+    p = sub.add_parser("sweep")
+    for fam in ("prolate", "randsvd", "mtx"):
+        p.add_argument(f"--{fam}", default=None)
+    p.add_argument("--methods", default="gmres-ir,rgmres-ir")
+    precision_flags(p), solver_flags(p)
+    p.add_argument("--jobs", type=int, default=1)
+    p.add_argument("--out", required=True)
+    p.add_argument("--format", default="csv", choices=("csv", "markdown", "json"))
+    p = sub.add_parser("kscan")
+    p.add_argument("--problem", required=True)
+    p.add_argument("--method", default="rgmres-ir")
+    precision_flags(p), solver_flags(p)
+    p.add_argument("--k-range", required=True)
+    p.add_argument("--out", required=True)
+    p.add_argument("--format", default="csv", choices=("csv", "markdown", "json"))
+    p = sub.add_parser("gen")
+    p.add_argument("--problem", required=True)
+    p.add_argument("--n", type=int, default=100)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--out", required=True)
+    return ap
+
+
+def _k_values(text: str) -> list:
+    if ":" in text:
+        lo, hi = text.split(":")
+        return list(range(int(lo), int(hi) + 1))
+    return [int(t) for t in text.split(",") if t.strip()]
+
+
+def main(argv=None) -> int:
+    """The reference CLI's solve / sweep / kscan / gen commands (harness.py:476-565)."""
+    args = _parser().parse_args(argv)
+    if getattr(args, "half_ftz", False):
+        set_half_flush_subnormals(True)
+    try:
+        if args.command == "gen":
+            ref = ProblemRef.parse(args.problem, n=args.n, seed=args.seed)
+            a, _ = ref.materialize()
+            write_matrix_market(args.out, a, comment=ref.problem_id)
+            print(f"wrote {ref.problem_id} ({a.shape[0]}x{a.shape[1]}) to {args.out}")
+            return 0
+        prec = PrecisionTriple.parse(args.uf, args.u, args.ur)
+        if args.command == "solve":
+            ref = ProblemRef.parse(args.problem, n=args.n, seed=args.seed)
+            a, b = ref.materialize()
+            rep = solve(a, b, RefineConfig(precisions=prec, method=Method.parse(args.method), m=args.m, k=args.k,
+                                           tau=args.tau, i_max=args.imax, scale_diag=args.scale_diag))
+            tail = "" if rep.converged else f"  [{rep.divergence_reason.value}]"
+            print(f"{ref.problem_id} {args.method}: {format_cell(rep)}  nbe={rep.nbe_final:.3e} "
+                  f"ferr={rep.ferr_final:.3e}{tail}")
+            if args.out:
+                with open(args.out, "w", encoding="ascii") as fh:
+                    fh.write(json.dumps(_payload(rep), indent=2) + "\n")
+            return 0
+        if args.command == "sweep":
+            refs = []
+            for fam, key in (("prolate", "alpha"), ("randsvd", "kappa2"), ("mtx", "path")):
+                for tok in (getattr(args, fam) or "").split(","):
+                    if tok.strip():
+                        val = tok.strip() if fam == "mtx" else float(tok)
+                        refs.append(ProblemRef(fam, n=args.n, seed=args.seed, **{key: val}))
+            spec = SweepSpec(problems=refs, methods=[Method.parse(t) for t in args.methods.split(",")],
+                             precisions=prec, m=args.m, k=args.k, tau=args.tau, i_max=args.imax,
+                             seed=args.seed, scale_diag=args.scale_diag, jobs=args.jobs)
+            rows = run_sweep(spec)
+            emit(rows, args.format, args.out)
+            for r in rows:
+                print(f"{r['problem_id']:>16} {r['method']:>10}: {r['cell']}")
+            return 0
+        if args.command == "kscan":
+            ref = ProblemRef.parse(args.problem, n=args.n, seed=args.seed)
+            cfg = RefineConfig(precisions=prec, method=Method.parse(args.method), m=args.m, tau=args.tau,
+                               i_max=args.imax, scale_diag=args.scale_diag)
+            rows = kscan(ref, cfg, _k_values(args.k_range))
+            emit(rows, args.format, args.out)
+            for r in rows:
+                print(f"k={r['k']:>3}  total={r['total_inner']}")
+            return 0
+    except (ValueError, OSError, NotImplementedError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 2
+    return 2
+
+
+if __name__ == "__main__":
+    sys.exit(main())

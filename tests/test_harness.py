@@ -145,3 +145,59 @@ def test_mtx_round_trip_and_sweep_problem(tmp_path):
     ref = harness.ProblemRef.parse(f"mtx:{path}")
     got, b = ref.materialize()
     assert ref.problem_id == "p45" and np.array_equal(got, a) and np.array_equal(b, np.ones(12))
+
+
+def _rows():
+    return [{"problem_id": "prolate:0.45", "kappa_inf": 1.5e9, "kappa_2": 1e9, "method": "gmres-ir", "m": 16,
+             "k": 0, "tau": 1e-8, "converged": True, "steps": 2, "total_inner": 15, "per_step": "7;8",
+             "nbe_final": 3.1e-17, "ferr_final": 0.0, "divergence_reason": "", "cell": "15 (7,8)", "report": None}]
+
+
+def test_emit_formats(tmp_path):
+    import json
+
+    p = tmp_path / "o.csv"
+    harness.emit(_rows(), "csv", p)
+    lines = p.read_text().splitlines()
+    assert lines[0] == ",".join(harness.CSV_COLUMNS)
+    assert lines[1] == "prolate:0.45,1500000000.0,1000000000.0,gmres-ir,16,0,1e-08,true,2,15,7;8,3.1e-17,0.0,"
+    harness.emit(_rows(), "markdown", p)
+    md = p.read_text().splitlines()
+    assert md[0] == "| problem_id | method | m | k | result | converged | nbe_final |"
+    assert md[2] == "| prolate:0.45 | gmres-ir | 16 | 0 | 15 (7,8) | true | 3.1e-17 |"
+    harness.emit([{"k": 4, "total_inner": 12}], "csv", p)
+    assert p.read_text() == "k,total_inner\n4,12\n"
+    harness.emit(_rows(), "json", p)
+    assert json.loads(p.read_text())[0]["cell"] == "15 (7,8)"
+    with pytest.raises(ValueError):
+        harness.emit(_rows(), "xml", p)
+
+
+def test_cli_gen_and_errors(tmp_path, capsys):
+    from paper_2201_09827_b200.mtx import read_matrix_market
+
+    out = str(tmp_path / "g.mtx")
+    assert harness.main(["gen", "--problem", "prolate:0.45", "--n", "10", "--out", out]) == 0
+    assert np.array_equal(read_matrix_market(out), harness.ProblemRef.parse("prolate:0.45", n=10).materialize()[0])
+    assert harness.main(["gen", "--problem", "toeplitz:1", "--out", out]) == 2
+    assert "error:" in capsys.readouterr().err
+    assert harness._k_values("2:5") == [2, 3, 4, 5] and harness._k_values("1,4,8") == [1, 4, 8]
+
+
+@pytest.mark.gpu
+def test_cli_sweep_on_device(gpu, tmp_path):
+    """`sweep` as in SURVEY Appendix A (Table 5 settings) writes the reference's
+    CSV columns; per-step counts match the reference's golden rows +-1."""
+    out = str(tmp_path / "t5.csv")
+    rc = harness.main(["sweep", "--prolate", "0.475,0.467", "--methods", "gmres-ir,rgmres-ir", "--uf", "single",
+                       "--u", "double", "--ur", "quad", "--m", "16", "--k", "4", "--tau", "1e-8", "--out", out])
+    assert rc == 0
+    lines = open(out).read().splitlines()
+    assert lines[0] == ",".join(harness.CSV_COLUMNS) and len(lines) == 5
+    gold = golden_json("table5")["rows"]
+    for line in lines[1:]:
+        f = dict(zip(harness.CSV_COLUMNS, line.split(",")))
+        want = next(r for r in gold if f"prolate:{r['alpha']:g}" == f["problem_id"] and r["method"] == f["method"])
+        per = [int(c) for c in f["per_step"].split(";")]
+        assert f["converged"] == "true" and len(per) == len(want["inner_iters"])
+        assert all(abs(x - y) <= 1 for x, y in zip(per, want["inner_iters"]))
