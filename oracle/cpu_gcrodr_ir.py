@@ -994,9 +994,23 @@ def forward_error(x, xref):
     return e if d == 0.0 else e / d
 
 
+def pow2_equilibrate(a, b):
+    """Row then column scaling by the power of two nearest 1/max|.|
+    (refine.py:261-270); exact in binary.  Returns (a', b', column scales)."""
+    rmax = np.max(np.abs(a), axis=1)
+    rmax = np.where(rmax == 0.0, 1.0, rmax)
+    r = np.exp2(-np.round(np.log2(rmax)))
+    ar = a * r[:, None]
+    cmax = np.max(np.abs(ar), axis=0)
+    cmax = np.where(cmax == 0.0, 1.0, cmax)
+    c = np.exp2(-np.round(np.log2(cmax)))
+    return ar * c[None, :], b * r, c
+
+
 def solve(a, b, precisions=("half", "single", "double"), method="rgmres-ir", m=0, k=0,
           tau=None, i_max=10000, extra_precision_matvec=None, c_conv=2.0, max_cycles=None,
-          reorthogonalize=True, restart_residual="recurrence", cycle_residual="recurrence") -> Report:
+          reorthogonalize=True, restart_residual="recurrence", cycle_residual="recurrence",
+          scale_diag=False) -> Report:
     """The shared refinement loop (refine.py:277-421) for every method."""
     uf, u, ur = precisions
     check_triple(uf, u, ur)
@@ -1013,11 +1027,16 @@ def solve(a, b, precisions=("half", "single", "double"), method="rgmres-ir", m=0
         if a.shape != (n, n) or b.shape != (n,):
             raise ValueError("need a square matrix and a matching right-hand side")
         diag: dict = {}
+        col_scale = None
+        if scale_diag:  # refine.py:293-297 with _pow2_equilibrate (261-270)
+            a, b, col_scale = pow2_equilibrate(a, b)
+            a, b = rnd(a, u), rnd(b, u)
+            diag["equilibrated"] = True
         norm_a, norm_b = inf_norm(a), inf_norm(b)
         try:
             F = lu_factor(a, uf)
         except ZeroPivot as exc:
-            return Report(False, 0, [], [], [], "InnerStagnation", None, {"lu_failed": str(exc)})
+            return Report(False, 0, [], [], [], "InnerStagnation", None, {"lu_failed": str(exc), **diag})
         diag["lu_growth"] = F.growth
         x = lu_solve(F, b, uf, store=u)
         if not np.all(np.isfinite(x)):
@@ -1071,5 +1090,7 @@ def solve(a, b, precisions=("half", "single", "double"), method="rgmres-ir", m=0
             if state == "diverged":
                 reason = why
                 break
+    if col_scale is not None and x is not None:
+        x = col_scale * x  # refine.py:408-409
     return Report(converged, len(inner), inner, nbe_h, ferr_h, None if converged else reason,
                   x, diag, calls)

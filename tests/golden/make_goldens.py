@@ -340,6 +340,32 @@ CASES = {
 }
 
 
+def case_scaled():
+    """scale_diag=True (refine.py:261-270, 293-297, 408-409) on badly row/column
+    scaled randsvd systems: D_r A D_c with D ~ 10^U(-6, 6) (not powers of two,
+    so the equilibration is not a no-op)."""
+    rng = np.random.default_rng(2201)
+    out = {}
+    for n, kappa, prec, method, m, k, tau in ((60, 1e3, ("half", "single", "double"), "rgmres-ir", 20, 4, 1e-4),
+                                              (80, 1e5, ("single", "double", "quad"), "gmres-ir", 30, 0, 1e-8)):
+        a0 = problems.randsvd(n, kappa, seed=7)
+        dr, dc = 10.0 ** rng.uniform(-6, 6, n), 10.0 ** rng.uniform(-6, 6, n)
+        a = dr[:, None] * a0 * dc[None, :]
+        b = rng.standard_normal(n)
+        tag = f"{prec[0]}_{method}"
+        cfg = refine.RefineConfig(precisions=precision.PrecisionTriple.parse(*prec),
+                                  method=refine.Method.parse(method), m=m, k=k, tau=tau, i_max=20, scale_diag=True)
+        rep = refine.solve(a, b, cfg)
+        d = _report_dict(rep)
+        d.update(precisions=list(prec), method=method, m=m, k=k, tau=tau, i_max=20, n=n)
+        out[tag] = (d, a, b)
+    _dump("scaled", {t: v[0] for t, v in out.items()},
+          {**{f"{t}_a": v[1] for t, v in out.items()}, **{f"{t}_b": v[2] for t, v in out.items()}})
+
+
+CASES["scaled"] = case_scaled
+
+
 if __name__ == "__main__":
     if os.environ.get("OPENBLAS_NUM_THREADS") != "1":
         sys.exit("set OPENBLAS_NUM_THREADS=1 (SURVEY.md F14)")

@@ -228,3 +228,23 @@ def test_sir_and_uniform_variants(gpu, method, prec):
     assert len(rep.inner_iters) == len(ref.inner_iters), (rep.inner_iters, ref.inner_iters)
     assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters, ref.inner_iters)
     assert _level_ok(rep.nbe_history[-1], ref.nbe_history[-1], 10.0, u * 0.05), (rep.nbe_history, ref.nbe_history)
+
+
+@pytest.mark.parametrize("tag", ["half_rgmres-ir", "single_gmres-ir"])
+def test_scale_diag(gpu, tag):
+    """scale_diag=True on systems scaled by 10^U(-6,6) per row and column,
+    against the reference's runs (tests/golden/make_goldens.py scaled)."""
+    from conftest import golden_npz
+
+    g = golden_json("scaled")[tag]
+    z = golden_npz("scaled")
+    cfg = RefineConfig(PrecisionTriple.parse(*g["precisions"]), Method.parse(g["method"]), m=g["m"], k=g["k"],
+                       tau=g["tau"], i_max=g["i_max"], scale_diag=True)
+    rep = _refine(z[f"{tag}_a"], z[f"{tag}_b"], cfg)
+    u = {"single": 2.0 ** -24, "double": 2.0 ** -53}[g["precisions"][1]]
+    assert rep.converged == g["converged"] and rep.diagnostics.get("equilibrated")
+    assert len(rep.inner_iters) == len(g["inner_iters"])
+    assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, g["inner_iters"])), (rep.inner_iters, g["inner_iters"])
+    assert _level_ok(rep.nbe_history[-1], g["nbe_history"][-1], 10.0, u * 0.05)
+    ref = np.array(g["solution"])
+    assert np.max(np.abs(rep.solution - ref)) <= 4 * u * np.max(np.abs(ref))

@@ -131,3 +131,17 @@ def test_config3_subset_golden():
             rep = O.solve(a, b, spec.precisions, method, spec.m, spec.k if method[0] == "r" else 0,
                           spec.tau, spec.i_max)
             _same_report(rep, g[method][i])
+
+
+@pytest.mark.parametrize("tag", ["half_rgmres-ir", "single_gmres-ir"])
+def test_scale_diag_matches_reference(tag):
+    """scale_diag=True (pow2 equilibration, refine.py:261-270, 293-297, 408-409)
+    on badly scaled systems: the oracle reproduces the reference run exactly."""
+    g = golden_json("scaled")[tag]
+    z = golden_npz("scaled")
+    rep = O.solve(z[f"{tag}_a"], z[f"{tag}_b"], tuple(g["precisions"]), g["method"], g["m"], g["k"], g["tau"],
+                  g["i_max"], scale_diag=True)
+    assert rep.converged == g["converged"] and rep.inner_iters == g["inner_iters"]
+    assert rep.nbe_history == g["nbe_history"]
+    assert np.array_equal(rep.solution, np.array(g["solution"]))
+    assert rep.diagnostics.get("equilibrated")
