@@ -30,7 +30,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 #   d_f_dd   (single, double, quad)   configs 2a, 4, Table 5
 #   d_h_dd   (half, double, double)   config 2b
 #   f_h_f32, d_f_f64, d_h_f64          uniform-precision (S-) variants
-DEFAULT_VARIANTS = ["f_h_f64", "d_f_dd", "d_h_dd", "f_h_f32", "d_f_f64", "d_h_f64"]
+#   d_d_f64  (double, double, double)  fp64 factors: harness.spectrum_dump
+DEFAULT_VARIANTS = ["f_h_f64", "d_f_dd", "d_h_dd", "f_h_f32", "d_f_f64", "d_h_f64", "d_d_f64"]
 ALL_VARIANTS = ["f_h_f64", "f_h_f32", "f_f_f64", "f_f_f32", "d_h_dd", "d_h_f64", "d_f_dd", "d_f_f64",
                 "d_d_dd", "d_d_f64"]
 

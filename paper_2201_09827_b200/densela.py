@@ -85,7 +85,8 @@ class LUFactors:
 
 
 def _context(a: np.ndarray, uf: Format, u: Format) -> _lib.Solver:
-    if _ORDER.index(u) <= _ORDER.index(uf) or u not in (Format.SINGLE, Format.DOUBLE):
+    wider = _ORDER.index(u) > _ORDER.index(uf) or u is uf is Format.DOUBLE  # fp64 factors: u = double
+    if not wider or u not in (Format.SINGLE, Format.DOUBLE):
         raise NotImplementedError(f"no device context stores {uf.value} factors at u = {u.value}")
     n = a.shape[0]
     ur = Format.DOUBLE

@@ -20,10 +20,11 @@ import numpy as np
 
 from . import problems
 from .mtx import read_matrix_market, write_matrix_market
-from .precision import PrecisionTriple, set_half_flush_subnormals
+from .precision import Format, PrecisionTriple, set_half_flush_subnormals
 from .refine import Method, RefineConfig, RefinementReport, solve
 
 __all__ = ["ProblemRef", "SweepSpec", "format_cell", "run_sweep", "kscan", "cond_inf", "emit", "main",
+           "spectrum_dump", "preconditioned_matrix",
            "CSV_COLUMNS"]
 
 # harness.py:55-70
@@ -195,6 +196,55 @@ def kscan(problem: ProblemRef, cfg: RefineConfig, k_range) -> list:
     return rows
 
 
+def preconditioned_matrix(a, factors) -> np.ndarray:
+    """U^-1 L^-1 P A in double, one device operator application per column
+    (harness.py:265-273 forms the same matrix by triangular solves)."""
+    from . import densela
+
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[0]
+    out = np.empty((n, n))
+    e = np.zeros(n)
+    for j in range(n):
+        e[j] = 1.0
+        out[:, j] = densela.apply_preconditioned(a, factors, e, Format.DOUBLE, Format.DOUBLE)
+        e[j] = 0.0
+    return out
+
+
+def spectrum_dump(a, uf_format: Format, out) -> list:
+    """Eigenvalues of A and of the double- and uf-preconditioned operators as
+    CSV points ``set,re,im`` (harness.py:276-303); returns the set names
+    written.  Factors and operator columns come from the device; the dense
+    eigensolve of the n x n result (n <= 500) is the host's LAPACK, as in the
+    reference (densela.py:435-457)."""
+    from . import densela
+
+    a = np.asarray(a, dtype=np.float64)
+    if a.shape[0] > 500:
+        raise ValueError("spectrum dump is limited to n <= 500")
+    sets = []
+
+    def add(name, mat):
+        try:
+            vals = np.linalg.eigvals(mat)
+        except np.linalg.LinAlgError:  # eig_small's NoConvergence: the set is skipped
+            return
+        sets.append((name, vals[np.argsort(np.abs(vals), kind="stable")]))
+
+    add("original", a)
+    for fmt in (Format.DOUBLE, uf_format):
+        f = densela.lu_factor(a, fmt)
+        try:
+            add(f"precond_{fmt.value}", preconditioned_matrix(a, f))
+        finally:
+            f.close()
+    lines = ["set,re,im"] + [f"{name},{float(v.real)!r},{float(v.imag)!r}" for name, vals in sets for v in vals]
+    with open(out, "w", encoding="ascii") as fh:
+        fh.write("\n".join(lines) + "\n")
+    return [name for name, _ in sets]
+
+
 # ---------------------------------------------------------------------------
 # serialisation and the command line (harness.py:335-565)
 # ---------------------------------------------------------------------------
@@ -269,6 +319,12 @@ def _parser() -> argparse.ArgumentParser:
     p.add_argument("--jobs", type=int, default=1)
     p.add_argument("--out", required=True)
     p.add_argument("--format", default="csv", choices=("csv", "markdown", "json"))
+    p = sub.add_parser("spectrum")
+    p.add_argument("--problem", required=True)
+    p.add_argument("--uf", default="half")
+    p.add_argument("--n", type=int, default=100)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--out", required=True)
     p = sub.add_parser("kscan")
     p.add_argument("--problem", required=True)
     p.add_argument("--method", default="rgmres-ir")
@@ -302,6 +358,11 @@ def main(argv=None) -> int:
             a, _ = ref.materialize()
             write_matrix_market(args.out, a, comment=ref.problem_id)
             print(f"wrote {ref.problem_id} ({a.shape[0]}x{a.shape[1]}) to {args.out}")
+            return 0
+        if args.command == "spectrum":
+            ref = ProblemRef.parse(args.problem, n=args.n, seed=args.seed)
+            names = spectrum_dump(ref.materialize()[0], Format.parse(args.uf), args.out)
+            print(f"wrote {len(names)} point sets to {args.out}")
             return 0
         prec = PrecisionTriple.parse(args.uf, args.u, args.ur)
         if args.command == "solve":

@@ -201,3 +201,38 @@ def test_cli_sweep_on_device(gpu, tmp_path):
         per = [int(c) for c in f["per_step"].split(";")]
         assert f["converged"] == "true" and len(per) == len(want["inner_iters"])
         assert all(abs(x - y) <= 1 for x, y in zip(per, want["inner_iters"]))
+
+
+def test_spectrum_dump_size_limit(tmp_path):
+    with pytest.raises(ValueError):
+        harness.spectrum_dump(np.eye(501), harness.Format.HALF, tmp_path / "s.csv")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("uf", ["half", "double"])
+def test_preconditioned_matrix_and_spectrum(gpu, uf, tmp_path):
+    """U^-1 L^-1 P A from device operator columns equals the matrix formed by
+    triangular solves on the oracle's factors (harness.py:265-273) to double
+    rounding x kappa; the dump writes the three point sets (harness.py:276-303)."""
+    import scipy.linalg as sl
+
+    from oracle import cpu_gcrodr_ir as O
+    from paper_2201_09827_b200 import densela
+
+    a = harness.ProblemRef.parse("randsvd:1e3", n=48).materialize()[0]
+    F = densela.lu_factor(a, harness.Format.parse(uf))
+    R = O.lu_factor(a, uf)
+    if uf == "half":
+        assert np.array_equal(F.perm, R.perm) and np.array_equal(F.U, R.U)
+    m = harness.preconditioned_matrix(a, F)
+    F.close()
+    want = sl.solve_triangular(F.U, sl.solve_triangular(F.L, a[F.perm], lower=True, unit_diagonal=True))
+    np.testing.assert_allclose(m, want, rtol=0, atol=1e3 * 2.0 ** -52 * np.max(np.abs(want)))
+    out = tmp_path / "s.csv"
+    names = harness.spectrum_dump(a, harness.Format.parse(uf), out)
+    assert names == ["original", "precond_double", f"precond_{uf}"] or names == ["original", "precond_double"]
+    lines = out.read_text().splitlines()
+    assert lines[0] == "set,re,im" and len(lines) == 1 + 48 * len(names)
+    orig = np.array([complex(float(l.split(",")[1]), float(l.split(",")[2])) for l in lines[1:49]])
+    ev = np.linalg.eigvals(a)
+    assert np.array_equal(orig, ev[np.argsort(np.abs(ev), kind="stable")])
