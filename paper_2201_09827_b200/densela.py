@@ -64,18 +64,20 @@ class LUFactors:
     def n(self) -> int:
         return self.L.shape[0]
 
-    def _device(self, u: Format) -> _lib.Solver:
-        """Device context holding A and these factors at working precision u."""
-        s = self._ctx.get(u)
+    def _device(self, u: Format, extra: bool | None = None) -> _lib.Solver:
+        """Device context holding A and these factors at working precision u,
+        its operator at u^2 (extra) or u."""
+        extra = _default_extra(self.format, u) if extra is None else extra
+        s = self._ctx.get((u, extra))
         if s is None:
             if not _exact_in(self._a, u):
                 raise NotImplementedError(f"A is not exactly representable at u = {u.value}; a device "
                                           "context there would factor a different matrix")
-            s = _context(self._a, self.format, u)
+            s = _context(self._a, self.format, u, extra)
             zero, _ = s.factorize()
             if zero >= 0:
                 raise ExactZeroPivot(zero)
-            self._ctx[u] = s
+            self._ctx[(u, extra)] = s
         return s
 
     def close(self) -> None:
@@ -84,13 +86,20 @@ class LUFactors:
         self._ctx.clear()
 
 
-def _context(a: np.ndarray, uf: Format, u: Format) -> _lib.Solver:
+def _default_extra(uf: Format, u: Format) -> bool:
+    """Operator at u^2 as on the solve path, except for fp64 factors at u =
+    double (the build compiles that variant with the fp64 operator only)."""
+    return not (uf is u is Format.DOUBLE)
+
+
+def _context(a: np.ndarray, uf: Format, u: Format, extra: bool | None = None) -> _lib.Solver:
     wider = _ORDER.index(u) > _ORDER.index(uf) or u is uf is Format.DOUBLE  # fp64 factors: u = double
     if not wider or u not in (Format.SINGLE, Format.DOUBLE):
         raise NotImplementedError(f"no device context stores {uf.value} factors at u = {u.value}")
     n = a.shape[0]
     ur = Format.DOUBLE
-    cfg = RefineConfig(PrecisionTriple(uf, u, ur), Method.GMRES_IR, m=min(n, 2))
+    extra = _default_extra(uf, u) if extra is None else extra
+    cfg = RefineConfig(PrecisionTriple(uf, u, ur), Method.GMRES_IR, m=min(n, 2), extra_precision_matvec=extra)
     s = _lib.Solver(n, make_options(cfg, n))
     s.set_system(a, np.zeros(n))
     return s
@@ -129,7 +138,7 @@ def lu_factor(a, ctx) -> LUFactors:
     L = np.tril(lu, -1) + np.eye(a.shape[0])
     U = np.triu(lu)
     f = LUFactors(L, U, perm, uf, float(growth), _a=a)
-    f._ctx[u] = s
+    f._ctx[(u, _default_extra(uf, u))] = s
     return f
 
 
@@ -161,13 +170,15 @@ def apply_preconditioned(a, f: LUFactors, v, matvec_ctx, store_fmt: Format) -> n
     if a is not f._a and not np.array_equal(a, f._a, equal_nan=True):
         raise NotImplementedError("the device operator uses the matrix the factors were computed from")
     v = _vec(v, f.n, "vector")
-    return f._device(store_fmt).apply_preconditioned(v, _fmt(matvec_ctx).code)
+    mv = _fmt(matvec_ctx)
+    return f._device(store_fmt, mv is not store_fmt).apply_preconditioned(v, mv.code)
 
 
 def precond_rhs(f: LUFactors, r, matvec_ctx, store_fmt: Format) -> np.ndarray:
     """fl_store(U^-1 L^-1 r[perm]) at ``matvec_ctx`` (densela.py:314-333)."""
     r = _vec(r, f.n, "vector")
-    return f._device(store_fmt).precond_rhs(r, _fmt(matvec_ctx).code)
+    mv = _fmt(matvec_ctx)
+    return f._device(store_fmt, mv is not store_fmt).precond_rhs(r, mv.code)
 
 
 def residual(a, x, b, ctx) -> np.ndarray:
