@@ -24,7 +24,7 @@ from .precision import Format, PrecisionTriple, set_half_flush_subnormals
 from .refine import Method, RefineConfig, RefinementReport, solve
 
 __all__ = ["ProblemRef", "SweepSpec", "format_cell", "run_sweep", "kscan", "cond_inf", "emit", "main",
-           "spectrum_dump", "preconditioned_matrix",
+           "spectrum_dump", "preconditioned_matrix", "run_sweep_ranks",
            "CSV_COLUMNS"]
 
 # harness.py:55-70
@@ -180,6 +180,26 @@ def run_sweep(spec: SweepSpec) -> list:
     for ref in spec.problems:
         rows.extend(_one_problem(spec, ref))
     return rows
+
+
+def run_sweep_ranks(spec: SweepSpec, group=None) -> list:
+    """``run_sweep`` with the problems dealt round-robin over the ranks of a
+    ``torch.distributed`` group (one process per GPU) -- the multi-GPU form
+    of the reference's process pool (harness.py:248-252).  Every rank returns
+    the full row list, in spec order; the only collective is the final
+    object gather of the rows."""
+    import torch.distributed as dist
+
+    if not spec.problems:
+        raise ValueError("empty problem set")
+    if not spec.methods:
+        raise ValueError("empty method list")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    mine = {i: _one_problem(spec, ref) for i, ref in enumerate(spec.problems) if i % world == rank}
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    merged = {i: rows for part in parts for i, rows in part.items()}
+    return [row for i in range(len(spec.problems)) for row in merged[i]]
 
 
 def kscan(problem: ProblemRef, cfg: RefineConfig, k_range) -> list:

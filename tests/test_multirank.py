@@ -66,3 +66,40 @@ def test_two_rank_sharding_and_timing():
     assert s0 == s1 == [0]
     # the whole-job time is the slowest rank's
     assert t0 == t1 == 2.5
+
+
+def _sweep_worker(rank: int, world: int, port: int, out):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_09827_b200 import harness
+        from paper_2201_09827_b200.precision import PrecisionTriple
+        from paper_2201_09827_b200.refine import Method
+
+        # mtx problems that do not exist: each rank records its own in-row
+        # errors without touching a GPU, so the deal + gather logic is what runs
+        refs = [harness.ProblemRef.parse(f"mtx:/nonexistent/p{i}_r.mtx") for i in range(5)]
+        spec = harness.SweepSpec(refs, [Method.GMRES_IR, Method.RGMRES_IR],
+                                 PrecisionTriple.parse("single", "double", "quad"), m=16, k=4)
+        rows = harness.run_sweep_ranks(spec)
+        out.put((rank, [(r["problem_id"], r["method"], r["k"]) for r in rows]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sweep_deal_and_gather():
+    """run_sweep_ranks: problems dealt round-robin, every rank gets all rows in
+    spec order (same order as the single-process run_sweep)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [(f"p{i}_r", m, k) for i in range(5) for m, k in (("gmres-ir", 0), ("rgmres-ir", 4))]
+    assert got[0] == want and got[1] == want
