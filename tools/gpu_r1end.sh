@@ -1,7 +1,7 @@
 # round-1 closing run: GPU parity suite, smoke, default bench (cfg2), cfg3 bench,
 # launch list of the default bench (ncu, after the bench itself exited 0)
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r1end
+O=gpurun_out/${R1END_DIR:-r1end}
 mkdir -p $O
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
