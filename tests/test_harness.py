@@ -236,3 +236,21 @@ def test_preconditioned_matrix_and_spectrum(gpu, uf, tmp_path):
     orig = np.array([complex(float(l.split(",")[1]), float(l.split(",")[2])) for l in lines[1:49]])
     ev = np.linalg.eigvals(a)
     assert np.array_equal(orig, ev[np.argsort(np.abs(ev), kind="stable")])
+
+
+@pytest.mark.gpu
+def test_cli_solve_and_kscan_on_device(gpu, tmp_path, capsys):
+    """`solve --out` writes the report payload; `kscan` writes k,total_inner rows."""
+    import json
+
+    rep = str(tmp_path / "r.json")
+    assert harness.main(["solve", "--problem", "prolate:0.475", "--method", "rgmres-ir", "--m", "16", "--k", "4",
+                         "--tau", "1e-8", "--out", rep]) == 0
+    d = json.load(open(rep))
+    assert d["converged"] and d["inner_iters"] == [2, 3] and len(d["solution"]) == 100
+    assert "prolate:0.475 rgmres-ir: 5 (2,3)" in capsys.readouterr().out
+    ks = str(tmp_path / "k.csv")
+    assert harness.main(["kscan", "--problem", "prolate:0.455", "--m", "16", "--tau", "1e-8", "--k-range", "2:4",
+                         "--out", ks]) == 0
+    lines = open(ks).read().splitlines()
+    assert lines[0] == "k,total_inner" and [l.split(",")[0] for l in lines[1:]] == ["2", "3", "4"]
