@@ -6,7 +6,7 @@ Run in the build container only (the reference does not exist on the GPU box):
         python tests/golden/make_goldens.py <case> [<case> ...]
 
 Cases: precision, lu, kernels, cfg1, cfg3, table5, table6, cfg2a, cfg2b, cfg4,
-cfg5_1024.  Each case writes ``tests/golden/<case>.json`` (+ ``.npz`` when
+cfg5_1024, scaled, explicit.  Each case writes ``tests/golden/<case>.json`` (+ ``.npz`` when
 arrays are needed).  Inputs come from ``paper_2201_09827_b200.problems``,
 which is itself pinned against ``irkit.matgen`` here (``check_matgen``).
 ``OPENBLAS_NUM_THREADS=1`` is required: the fp32 LU pivots and fp64 GEMV bits
@@ -364,6 +364,24 @@ def case_scaled():
 
 
 CASES["scaled"] = case_scaled
+
+
+def case_explicit():
+    """restart_residual / cycle_residual = "explicit" (gmres.py:292-295,
+    gcrodr.py:301-304, 376-379) on config 1 with short restarts."""
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    out = {}
+    for method, m, k in (("gmres-ir", 4, 0), ("rgmres-ir", 4, 2), ("gmres-ir", 8, 0), ("rgmres-ir", 8, 3)):
+        cfg = refine.RefineConfig(precisions=precision.PrecisionTriple.parse("half", "single", "double"),
+                                  method=refine.Method.parse(method), m=m, k=k, tau=1e-4, i_max=10,
+                                  restart_residual="explicit", cycle_residual="explicit")
+        d = _report_dict(refine.solve(a, b, cfg))
+        d.update(method=method, m=m, k=k, tau=1e-4, i_max=10)
+        out[f"{method}_m{m}"] = d
+    _dump("explicit", out)
+
+
+CASES["explicit"] = case_explicit
 
 
 if __name__ == "__main__":

@@ -145,3 +145,18 @@ def test_scale_diag_matches_reference(tag):
     assert rep.nbe_history == g["nbe_history"]
     assert np.array_equal(rep.solution, np.array(g["solution"]))
     assert rep.diagnostics.get("equilibrated")
+
+
+@pytest.mark.parametrize("tag", ["gmres-ir_m4", "rgmres-ir_m4", "gmres-ir_m8", "rgmres-ir_m8"])
+def test_explicit_residual_matches_reference(tag):
+    """restart_residual / cycle_residual = "explicit": the oracle reproduces the
+    reference's runs exactly (the checker of the GPU explicit-residual tests)."""
+    from paper_2201_09827_b200 import problems
+
+    g = golden_json("explicit")[tag]
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    rep = O.solve(a, b, ("half", "single", "double"), g["method"], g["m"], g["k"], g["tau"], g["i_max"],
+                  restart_residual="explicit", cycle_residual="explicit")
+    assert rep.converged == g["converged"] and rep.inner_iters == g["inner_iters"]
+    assert rep.nbe_history == g["nbe_history"]
+    assert np.array_equal(rep.solution, np.array(g["solution"]))
