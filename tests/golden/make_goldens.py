@@ -6,7 +6,7 @@ Run in the build container only (the reference does not exist on the GPU box):
         python tests/golden/make_goldens.py <case> [<case> ...]
 
 Cases: precision, lu, kernels, cfg1, cfg3, table5, table6, cfg2a, cfg2b, cfg4,
-cfg5_1024, scaled, explicit.  Each case writes ``tests/golden/<case>.json`` (+ ``.npz`` when
+cfg5_1024, scaled, explicit, variants.  Each case writes ``tests/golden/<case>.json`` (+ ``.npz`` when
 arrays are needed).  Inputs come from ``paper_2201_09827_b200.problems``,
 which is itself pinned against ``irkit.matgen`` here (``check_matgen``).
 ``OPENBLAS_NUM_THREADS=1`` is required: the fp32 LU pivots and fp64 GEMV bits
@@ -382,6 +382,27 @@ def case_explicit():
 
 
 CASES["explicit"] = case_explicit
+
+
+def case_variants():
+    """SIR and the uniform-precision S-variants (refine.py:56-83, 124-131,
+    378-380) on config 1 under three precision triples."""
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    out = {}
+    for prec in (("half", "single", "double"), ("single", "double", "double"), ("half", "double", "double")):
+        for method in ("sir", "sgmres-ir", "rsgmres-ir"):
+            m = 0 if method == "sir" else 100
+            k = 5 if method == "rsgmres-ir" else 0
+            tau = None if method == "sir" else 1e-4
+            cfg = refine.RefineConfig(precisions=precision.PrecisionTriple.parse(*prec),
+                                      method=refine.Method.parse(method), m=m, k=k, tau=tau, i_max=10)
+            d = _report_dict(refine.solve(a, b, cfg))
+            d.update(precisions=list(prec), method=method, m=m, k=k, tau=tau, i_max=10)
+            out[f"{prec[0]}_{prec[1]}_{method}"] = d
+    _dump("variants", out)
+
+
+CASES["variants"] = case_variants
 
 
 if __name__ == "__main__":

@@ -160,3 +160,20 @@ def test_explicit_residual_matches_reference(tag):
     assert rep.converged == g["converged"] and rep.inner_iters == g["inner_iters"]
     assert rep.nbe_history == g["nbe_history"]
     assert np.array_equal(rep.solution, np.array(g["solution"]))
+
+
+_VARIANT_TAGS = [f"{p}_{m}" for p in ("half_single", "single_double", "half_double")
+                 for m in ("sir", "sgmres-ir", "rsgmres-ir")]
+
+
+@pytest.mark.parametrize("tag", _VARIANT_TAGS)
+def test_sir_and_s_variants_match_reference(tag):
+    """SIR / SGMRES-IR / RSGMRES-IR on config 1 (tests/golden/variants.json,
+    reference runs): verdict, reason, per-step counts and every nbe exact."""
+    from paper_2201_09827_b200 import problems
+
+    g = golden_json("variants")[tag]
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    rep = O.solve(a, b, tuple(g["precisions"]), g["method"], g["m"], g["k"], g["tau"], g["i_max"])
+    assert rep.converged == g["converged"] and rep.divergence_reason == g["divergence_reason"]
+    assert rep.inner_iters == g["inner_iters"] and rep.nbe_history == g["nbe_history"]
