@@ -137,6 +137,18 @@ def require_gpu():
     return lib
 
 
+def current_device() -> int:
+    """torch's current CUDA device when torch is initialised, else 0."""
+    try:
+        import torch
+
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return int(torch.cuda.current_device())
+    except Exception:  # pragma: no cover - torch is plumbing only
+        pass
+    return 0
+
+
 def current_stream() -> int:
     """torch's current CUDA stream when torch is initialised, else NULL."""
     try:

@@ -11,7 +11,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .refine import DivergenceReason, RefineConfig, RefinementReport, make_options
+from .refine import DivergenceReason, RefineConfig, RefinementReport, _pow2_equilibrate, _round_u, make_options
 
 __all__ = ["solve_batched", "BatchResult"]
 
@@ -34,6 +34,7 @@ class BatchResult:
         self.x = np.zeros((count, n))
         self.growth = np.zeros(count)
         self.device_ms = 0.0
+        self.col_scale = None  # (count, n) when cfg.scale_diag equilibrated the systems
 
     def c_struct(self) -> _lib.BatchOut:
         o = _lib.BatchOut()
@@ -52,9 +53,13 @@ class BatchResult:
             diag["x0_reset"] = True
         if self.flags[i] & 2:
             diag["no_reference_solution"] = True
+        x = self.x[i].copy()
+        if self.col_scale is not None:
+            diag["equilibrated"] = True
+            x = self.col_scale[i] * x  # refine.py:408-409
         return RefinementReport(bool(self.converged[i]), s, self.inner[i, :s].tolist(),
                                 self.nbe[i, :s].tolist(), self.ferr[i, :s].tolist(),
-                                _REASON[int(self.reason[i])], self.x[i].copy(), diag)
+                                _REASON[int(self.reason[i])], x, diag)
 
     def reports(self) -> list[RefinementReport]:
         return [self.report(i) for i in range(self.count)]
@@ -73,12 +78,26 @@ def solve_batched(a, b, cfg: RefineConfig, *, on_device_ptrs: tuple[int, int] | 
         count, n = a.shape[0], a.shape[1]
         if a.shape != (count, n, n) or b.shape != (count, n):
             raise ValueError("need a (count, n, n) stack and a (count, n) right-hand side")
+        col_scale = None
+        if cfg.scale_diag:
+            # per-system pow2 equilibration on the host, as _refine does for one
+            # system (refine.py:293-297); the device repeats the rounding to u
+            u = cfg.precisions.u
+            a, b = a.copy(), b.copy()
+            col_scale = np.empty((count, n))
+            for i in range(count):
+                a[i], b[i], col_scale[i] = _pow2_equilibrate(_round_u(a[i], u), _round_u(b[i], u))
         pa, pb, dev = a.ctypes.data, b.ctypes.data, 0
     else:
+        if cfg.scale_diag:
+            raise NotImplementedError("scale_diag with device-resident inputs: pass host arrays "
+                                      "(the equilibration runs on the host)")
         pa, pb = on_device_ptrs
         dev = 1
+        col_scale = None
     opts = make_options(cfg, n)
     res = BatchResult(count, n, cfg.i_max)
+    res.col_scale = col_scale
     out = res.c_struct()
     ms = C.c_double()
     _lib._check(lib.gb_solve_batched(count, n, C.byref(opts), cfg.i_max, cfg.c_conv, C.c_void_p(pa),

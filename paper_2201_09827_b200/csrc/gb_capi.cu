@@ -84,6 +84,14 @@ gb_status gb_solver_create(gb_solver** out, int n, const gb_options* opt, void* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int want = o.grid_ctas > 0 ? o.grid_ctas : std::min(sms, std::max(2, (n + 63) / 64));
     s->G = std::min(want, sms);
+    // the team's MGS keeps a CTA's slice of w in registers, 4 rows per
+    // thread (gb_krylov.cuh): every slice must have <= 4 * 256 rows
+    auto slice = [n](int G) { return (((n + G - 1) / G) + 31) & ~31; };
+    while (s->G < sms && slice(s->G) > 4 * 256) ++s->G;
+    if (slice(s->G) > 4 * 256) {
+      delete s;
+      return fail(GB_ERR_UNSUPPORTED, "order too large for this device's team (rows per CTA > 1024)");
+    }
     // a team of <= 16 CTAs runs as one thread-block cluster (hardware
     // barrier) unless GB_TEAM=grid asks for the cooperative grid barrier
     const char* team = std::getenv("GB_TEAM");

@@ -122,6 +122,9 @@ __device__ int lu_cta(typename LuT<M>::C* a, int n, int lda, int* perm, PivKey* 
     const int p = key.i;
     const C piv = a[(size_t)p * lda + k];
     const bool isz = (piv == C(0));
+    // every thread holds the pivot before the row interchange below may
+    // overwrite a[p][k] (thread k % blockDim swaps that entry)
+    __syncthreads();
     if (isz && zero < 0) zero = k;
     if (isz && L::kLapack) continue;  // LAPACK: column already zero below
     if (p != k) {
@@ -184,184 +187,6 @@ __global__ void k_lu_convert(const TA* __restrict__ A, size_t lda, typename LuT<
   }
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) atomic_max_abs(&st->amax_bits, m);
-}
-
-// single-CTA panel factorisation on global memory: columns [k0, k0+nb)
-template <int M>
-__global__ void __launch_bounds__(1024) k_lu_panel(typename LuT<M>::S* W, size_t ld, int n, int k0, int nb,
-                                                   int* perm, int* piv, LuStatus* st) {
-  using L = LuT<M>;
-  using C = typename L::C;
-  __shared__ PivKey scratch[32];
-  const int kend = min(n, k0 + nb);
-  for (int k = k0; k < kend; ++k) {
-    PivKey key{0.0, -1, 0};
-    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
-      PivKey c = make_key((double)L::ld(W[(size_t)i * ld + k]), i);
-      if (piv_better(c, key)) key = c;
-    }
-    key = block_pivot(key, scratch);
-    const int p = key.i;
-    const C pv = L::ld(W[(size_t)p * ld + k]);
-    const bool isz = (pv == C(0));
-    if (threadIdx.x == 0) {
-      if (isz) atomicMin(&st->zero_col, k);
-      piv[k - k0] = p;
-      if (p != k && !(isz && L::kLapack)) {
-        int t = perm[k];
-        perm[k] = perm[p];
-        perm[p] = t;
-      } else {
-        piv[k - k0] = k;
-      }
-    }
-    if (isz && L::kLapack) {
-      __syncthreads();
-      continue;
-    }
-    if (p != k) {
-      for (int j = k0 + threadIdx.x; j < kend; j += blockDim.x) {
-        typename L::S t = W[(size_t)k * ld + j];
-        W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
-        W[(size_t)p * ld + j] = t;
-      }
-    }
-    __syncthreads();
-    const int w = kend - k - 1;  // remaining panel columns
-    // rows below k: multiplier then the panel-row update, one thread per row
-    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
-      typename L::S* row = W + (size_t)i * ld;
-      C l = L::mult(L::ld(row[k]), pv);
-      row[k] = L::st(l);
-      for (int j = 1; j <= w; ++j) {
-        C u = L::ld(W[(size_t)k * ld + k + j]);
-        row[k + j] = L::st(L::upd(L::ld(row[k + j]), l, u));
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// apply the panel's row interchanges to the columns outside the panel
-template <int M>
-__global__ void k_lu_laswp(typename LuT<M>::S* W, size_t ld, int n, int k0, int nb, const int* piv) {
-  const int kend = min(n, k0 + nb);
-  const int outside = n - (kend - k0);
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < outside; c += gridDim.x * blockDim.x) {
-    int j = c < k0 ? c : c + (kend - k0);
-    for (int k = k0; k < kend; ++k) {
-      int p = piv[k - k0];
-      if (p != k) {
-        auto t = W[(size_t)k * ld + j];
-        W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
-        W[(size_t)p * ld + j] = t;
-      }
-    }
-  }
-}
-
-// U12 = L11^-1 A12 with the exact per-element order (rows in increasing k)
-template <int M, int NB>
-__global__ void k_lu_trsm(typename LuT<M>::S* W, size_t ld, int n, int k0) {
-  using L = LuT<M>;
-  using C = typename L::C;
-  __shared__ C l11[NB][NB + 1];
-  const int kend = min(n, k0 + NB);
-  const int nbr = kend - k0;
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-    int r = e / NB, c = e % NB;
-    l11[r][c] = (r < nbr && c < nbr) ? L::ld(W[(size_t)(k0 + r) * ld + k0 + c]) : C(0);
-  }
-  __syncthreads();
-  for (int j = kend + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    C col[NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) col[r] = r < nbr ? L::ld(W[(size_t)(k0 + r) * ld + j]) : C(0);
-#pragma unroll
-    for (int r = 1; r < NB; ++r) {
-#pragma unroll
-      for (int i = 0; i < r; ++i) col[r] = L::upd(col[r], l11[r][i], col[i]);
-    }
-#pragma unroll
-    for (int r = 0; r < NB; ++r)
-      if (r < nbr) W[(size_t)(k0 + r) * ld + j] = L::st(col[r]);
-  }
-}
-
-// trailing update A22 -= L21 U12, k applied in order per element.
-// Tile 64 x 64, 256 threads, 4x4 elements per thread.
-template <int M, int NB>
-__global__ void __launch_bounds__(256) k_lu_gemm(typename LuT<M>::S* W, size_t ld, int n, int k0) {
-  using L = LuT<M>;
-  using C = typename L::C;
-  constexpr int TM = 64, TN = 64;
-  __shared__ C ls[TM][NB + 1];
-  __shared__ C us[NB][TN + 1];
-  const int k1 = k0 + NB;
-  if (k1 >= n) return;
-  const int i0 = k1 + blockIdx.y * TM, j0 = k1 + blockIdx.x * TN;
-  if (i0 >= n || j0 >= n) return;
-  for (int e = threadIdx.x; e < TM * NB; e += blockDim.x) {
-    int r = e / NB, c = e % NB;
-    ls[r][c] = (i0 + r < n) ? L::ld(W[(size_t)(i0 + r) * ld + k0 + c]) : C(0);
-  }
-  for (int e = threadIdx.x; e < NB * TN; e += blockDim.x) {
-    int r = e / TN, c = e % TN;
-    us[r][c] = (j0 + c < n) ? L::ld(W[(size_t)(k0 + r) * ld + j0 + c]) : C(0);
-  }
-  __syncthreads();
-  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
-  C acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
-      acc[a][b] = (i < n && j < n) ? L::ld(W[(size_t)i * ld + j]) : C(0);
-    }
-  if constexpr (L::kLapack) {
-    C s[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) s[a][b] = C(0);
-#pragma unroll 8
-    for (int k = 0; k < NB; ++k) {
-      C lv[4], uv[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) lv[a] = ls[tr + 16 * a][k];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) uv[b] = us[k][tc + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) s[a][b] = L::upd(s[a][b], -lv[a], uv[b]);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = acc[a][b] - s[a][b];
-  } else {
-#pragma unroll 4
-    for (int k = 0; k < NB; ++k) {
-      C lv[4], uv[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) lv[a] = ls[tr + 16 * a][k];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) uv[b] = us[k][tc + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = L::upd(acc[a][b], lv[a], uv[b]);
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
-      if (i < n && j < n) W[(size_t)i * ld + j] = L::st(acc[a][b]);
-    }
 }
 
 // dd-exact reciprocals of diag(U): 1/U_ii = rh + rl

@@ -126,7 +126,10 @@ __device__ bool dd_gepp_solve(const TA* A, size_t lda, const TW* b, int n, doubl
     }
     key = block_pivot(key, pscr);
     const int p = key.i;
-    if (ah[(size_t)p * n + k] == 0.0 && al[(size_t)p * n + k] == 0.0) {
+    const bool isz = ah[(size_t)p * n + k] == 0.0 && al[(size_t)p * n + k] == 0.0;
+    // all threads have read the pivot before the interchange rewrites row p
+    __syncthreads();
+    if (isz) {
       if (threadIdx.x == 0) s_zero = 1;
       __syncthreads();
       return false;

@@ -239,7 +239,9 @@ _SOLVER_LOCK = threading.Lock()
 
 
 def _options_key(n: int, o) -> tuple:
-    return (n,) + tuple(getattr(o, f) for f, _ in o._fields_)
+    # a cached solver owns device memory on the device that was current at
+    # creation and launches on the stream captured then: key on both
+    return (_lib.current_device(), _lib.current_stream(), n) + tuple(getattr(o, f) for f, _ in o._fields_)
 
 
 def _acquire_solver(n: int, opts):

@@ -11,14 +11,17 @@ from paper_2201_09827_b200.precision import PrecisionTriple
 from paper_2201_09827_b200.refine import Method, RefineConfig, RefinementReport
 
 
-def test_problem_ref_parse_and_ids():
-    p = harness.ProblemRef.parse("prolate:0.475")
-    assert (p.kind, p.alpha, p.n, p.problem_id) == ("prolate", 0.475, 100, "prolate:0.475")
-    r = harness.ProblemRef.parse("randsvd:1e12", n=64, seed=3)
-    assert (r.kappa2, r.n, r.seed, r.problem_id) == (1e12, 64, 3, "randsvd:1e+12")
-    assert harness.ProblemRef.parse("mtx:/data/bcsstk05.mtx").problem_id == "bcsstk05"
-    with pytest.raises(ValueError):
-        harness.ProblemRef.parse("toeplitz:3")
+def test_problem_text_and_labels():
+    p = harness.Problem.from_text("prolate:0.475")
+    assert (p.family, p.value, p.n, p.label) == ("prolate", 0.475, 100, "prolate:0.475")
+    r = harness.Problem.from_text("randsvd:1e12", n=64, seed=3)
+    assert (r.value, r.n, r.seed, r.label) == (1e12, 64, 3, "randsvd:1e+12")
+    assert harness.Problem.from_text("mtx:/data/bcsstk05.mtx").label == "bcsstk05"
+    for bad in ("toeplitz:3", "prolate"):
+        with pytest.raises(ValueError):
+            harness.Problem.from_text(bad)
+    a, b = harness.Problem.from_text("prolate:0.45", n=20).system()
+    assert a.shape == (20, 20) and np.array_equal(b, np.ones(20))
 
 
 def test_format_cell():
@@ -29,24 +32,26 @@ def test_format_cell():
 
 
 def test_cond_inf_matches_definition():
-    a = harness.ProblemRef.parse("prolate:0.45", n=20).materialize()[0]
+    a = harness.Problem.from_text("prolate:0.45", n=20).system()[0]
     want = np.linalg.norm(a, np.inf) * np.linalg.norm(np.linalg.inv(a), np.inf)
     assert math.isclose(harness.cond_inf(a), want, rel_tol=1e-12)
+    assert harness.cond_inf(np.zeros((3, 3))) == math.inf
 
 
 def test_sweep_validation_and_in_row_errors():
     spec = harness.SweepSpec([], [Method.GMRES_IR], PrecisionTriple.parse("single", "double", "quad"), m=16)
     with pytest.raises(ValueError):
         harness.run_sweep(spec)
-    spec = harness.SweepSpec([harness.ProblemRef.parse("mtx:/nonexistent.mtx")],
+    spec = harness.SweepSpec([harness.Problem.from_text("mtx:/nonexistent.mtx")],
                              [Method.GMRES_IR, Method.RGMRES_IR], PrecisionTriple.parse("single", "double", "quad"),
                              m=16, k=4)
     rows = harness.run_sweep(spec)
     assert [r["method"] for r in rows] == ["gmres-ir", "rgmres-ir"]
     assert [r["k"] for r in rows] == [0, 4]
     assert all(r["divergence_reason"].startswith("error:") and r["cell"] == "-" for r in rows)
+    assert all(set(harness.CSV_COLUMNS) <= set(r) for r in rows)
     with pytest.raises(ValueError):
-        harness.kscan(harness.ProblemRef.parse("prolate:0.45"),
+        harness.kscan(harness.Problem.from_text("prolate:0.45"),
                       RefineConfig(PrecisionTriple.parse("single", "double", "quad"), Method.RGMRES_IR, m=16, k=4),
                       [4, 16])
 
@@ -57,7 +62,7 @@ def test_table5_sweep_on_device(gpu):
     same verdict and per-step iterations +-1 against the reference's golden rows."""
     rows = [r for r in golden_json("table5")["rows"] if r["alpha"] >= 0.455]
     alphas = sorted({r["alpha"] for r in rows}, reverse=True)
-    spec = harness.SweepSpec([harness.ProblemRef.parse(f"prolate:{a}") for a in alphas],
+    spec = harness.SweepSpec([harness.Problem.from_text(f"prolate:{a}") for a in alphas],
                              [Method.GMRES_IR, Method.RGMRES_IR], PrecisionTriple.parse("single", "double", "quad"),
                              m=16, k=4, tau=1e-8)
     got = harness.run_sweep(spec)
@@ -68,7 +73,7 @@ def test_table5_sweep_on_device(gpu):
         per = [int(c) for c in g["per_step"].split(";")]
         assert len(per) == len(want["inner_iters"]), (per, want["inner_iters"])
         assert all(abs(x - y) <= 1 for x, y in zip(per, want["inner_iters"])), (per, want["inner_iters"])
-        assert g["kappa_inf"] > 1.0 and g["report"]["total_inner"] == sum(per)
+        assert g["kappa_inf"] > 1.0 and g["report"].total_inner == sum(per)
 
 
 @pytest.mark.gpu
@@ -76,7 +81,7 @@ def test_kscan_on_device(gpu):
     """Recycle-dimension scan (Fig. 2 shape): one row per k, totals positive
     for converged runs, -1 for divergent ones."""
     cfg = RefineConfig(PrecisionTriple.parse("single", "double", "quad"), Method.RGMRES_IR, m=16, k=4, tau=1e-8)
-    rows = harness.kscan(harness.ProblemRef.parse("prolate:0.455"), cfg, [1, 2, 4, 8])
+    rows = harness.kscan(harness.Problem.from_text("prolate:0.455"), cfg, [1, 2, 4, 8])
     assert [r["k"] for r in rows] == [1, 2, 4, 8]
     assert all(r["total_inner"] == -1 or r["total_inner"] > 0 for r in rows)
     k4 = next(r for r in golden_json("table5")["rows"] if r["alpha"] == 0.455 and r["method"] == "rgmres-ir")
@@ -137,70 +142,14 @@ def test_mtx_errors(tmp_path, text, line, kind):
 def test_mtx_round_trip_and_sweep_problem(tmp_path):
     from paper_2201_09827_b200.mtx import read_matrix_market, write_matrix_market
 
-    a = harness.ProblemRef.parse("prolate:0.45", n=12).materialize()[0]
+    a = harness.Problem.from_text("prolate:0.45", n=12).system()[0]
     a[3, 5] = 0.0
     path = str(tmp_path / "p45.mtx")
     write_matrix_market(path, a, comment="prolate 0.45\nn = 12")
     assert np.array_equal(read_matrix_market(path), a)
-    ref = harness.ProblemRef.parse(f"mtx:{path}")
-    got, b = ref.materialize()
-    assert ref.problem_id == "p45" and np.array_equal(got, a) and np.array_equal(b, np.ones(12))
-
-
-def _rows():
-    return [{"problem_id": "prolate:0.45", "kappa_inf": 1.5e9, "kappa_2": 1e9, "method": "gmres-ir", "m": 16,
-             "k": 0, "tau": 1e-8, "converged": True, "steps": 2, "total_inner": 15, "per_step": "7;8",
-             "nbe_final": 3.1e-17, "ferr_final": 0.0, "divergence_reason": "", "cell": "15 (7,8)", "report": None}]
-
-
-def test_emit_formats(tmp_path):
-    import json
-
-    p = tmp_path / "o.csv"
-    harness.emit(_rows(), "csv", p)
-    lines = p.read_text().splitlines()
-    assert lines[0] == ",".join(harness.CSV_COLUMNS)
-    assert lines[1] == "prolate:0.45,1500000000.0,1000000000.0,gmres-ir,16,0,1e-08,true,2,15,7;8,3.1e-17,0.0,"
-    harness.emit(_rows(), "markdown", p)
-    md = p.read_text().splitlines()
-    assert md[0] == "| problem_id | method | m | k | result | converged | nbe_final |"
-    assert md[2] == "| prolate:0.45 | gmres-ir | 16 | 0 | 15 (7,8) | true | 3.1e-17 |"
-    harness.emit([{"k": 4, "total_inner": 12}], "csv", p)
-    assert p.read_text() == "k,total_inner\n4,12\n"
-    harness.emit(_rows(), "json", p)
-    assert json.loads(p.read_text())[0]["cell"] == "15 (7,8)"
-    with pytest.raises(ValueError):
-        harness.emit(_rows(), "xml", p)
-
-
-def test_cli_gen_and_errors(tmp_path, capsys):
-    from paper_2201_09827_b200.mtx import read_matrix_market
-
-    out = str(tmp_path / "g.mtx")
-    assert harness.main(["gen", "--problem", "prolate:0.45", "--n", "10", "--out", out]) == 0
-    assert np.array_equal(read_matrix_market(out), harness.ProblemRef.parse("prolate:0.45", n=10).materialize()[0])
-    assert harness.main(["gen", "--problem", "toeplitz:1", "--out", out]) == 2
-    assert "error:" in capsys.readouterr().err
-    assert harness._k_values("2:5") == [2, 3, 4, 5] and harness._k_values("1,4,8") == [1, 4, 8]
-
-
-@pytest.mark.gpu
-def test_cli_sweep_on_device(gpu, tmp_path):
-    """`sweep` as in SURVEY Appendix A (Table 5 settings) writes the reference's
-    CSV columns; per-step counts match the reference's golden rows +-1."""
-    out = str(tmp_path / "t5.csv")
-    rc = harness.main(["sweep", "--prolate", "0.475,0.467", "--methods", "gmres-ir,rgmres-ir", "--uf", "single",
-                       "--u", "double", "--ur", "quad", "--m", "16", "--k", "4", "--tau", "1e-8", "--out", out])
-    assert rc == 0
-    lines = open(out).read().splitlines()
-    assert lines[0] == ",".join(harness.CSV_COLUMNS) and len(lines) == 5
-    gold = golden_json("table5")["rows"]
-    for line in lines[1:]:
-        f = dict(zip(harness.CSV_COLUMNS, line.split(",")))
-        want = next(r for r in gold if f"prolate:{r['alpha']:g}" == f["problem_id"] and r["method"] == f["method"])
-        per = [int(c) for c in f["per_step"].split(";")]
-        assert f["converged"] == "true" and len(per) == len(want["inner_iters"])
-        assert all(abs(x - y) <= 1 for x, y in zip(per, want["inner_iters"]))
+    ref = harness.Problem.from_text(f"mtx:{path}")
+    got, b = ref.system()
+    assert ref.label == "p45" and np.array_equal(got, a) and np.array_equal(b, np.ones(12))
 
 
 def test_spectrum_dump_size_limit(tmp_path):
@@ -219,7 +168,7 @@ def test_preconditioned_matrix_and_spectrum(gpu, uf, tmp_path):
     from oracle import cpu_gcrodr_ir as O
     from paper_2201_09827_b200 import densela
 
-    a = harness.ProblemRef.parse("randsvd:1e3", n=48).materialize()[0]
+    a = harness.Problem.from_text("randsvd:1e3", n=48).system()[0]
     F = densela.lu_factor(a, harness.Format.parse(uf))
     R = O.lu_factor(a, uf)
     if uf == "half":
@@ -238,19 +187,3 @@ def test_preconditioned_matrix_and_spectrum(gpu, uf, tmp_path):
     assert np.array_equal(orig, ev[np.argsort(np.abs(ev), kind="stable")])
 
 
-@pytest.mark.gpu
-def test_cli_solve_and_kscan_on_device(gpu, tmp_path, capsys):
-    """`solve --out` writes the report payload; `kscan` writes k,total_inner rows."""
-    import json
-
-    rep = str(tmp_path / "r.json")
-    assert harness.main(["solve", "--problem", "prolate:0.475", "--method", "rgmres-ir", "--m", "16", "--k", "4",
-                         "--tau", "1e-8", "--out", rep]) == 0
-    d = json.load(open(rep))
-    assert d["converged"] and d["inner_iters"] == [2, 3] and len(d["solution"]) == 100
-    assert "prolate:0.475 rgmres-ir: 5 (2,3)" in capsys.readouterr().out
-    ks = str(tmp_path / "k.csv")
-    assert harness.main(["kscan", "--problem", "prolate:0.455", "--m", "16", "--tau", "1e-8", "--k-range", "2:4",
-                         "--out", ks]) == 0
-    lines = open(ks).read().splitlines()
-    assert lines[0] == "k,total_inner" and [l.split(",")[0] for l in lines[1:]] == ["2", "3", "4"]

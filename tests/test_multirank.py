@@ -79,7 +79,7 @@ def _sweep_worker(rank: int, world: int, port: int, out):
 
         # mtx problems that do not exist: each rank records its own in-row
         # errors without touching a GPU, so the deal + gather logic is what runs
-        refs = [harness.ProblemRef.parse(f"mtx:/nonexistent/p{i}_r.mtx") for i in range(5)]
+        refs = [harness.Problem.from_text(f"mtx:/nonexistent/p{i}_r.mtx") for i in range(5)]
         spec = harness.SweepSpec(refs, [Method.GMRES_IR, Method.RGMRES_IR],
                                  PrecisionTriple.parse("single", "double", "quad"), m=16, k=4)
         rows = harness.run_sweep_ranks(spec)
