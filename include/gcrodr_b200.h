@@ -133,6 +133,11 @@ gb_status gb_time_op(gb_solver* s, int what, int reps, double* ms_per_launch);
  * (1 + 2*cap words: count, then pairs) out.  cap = 0 disarms. */
 gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out);
 
+/* diagnostics: the Hessenberg matrix H of the last Arnoldi cycle, (m+1) x m
+ * column-major fp64 (arnoldi_cycle's H, gmres.py:123-215); for per-cycle
+ * parity checks run the step with max_cycles = 1.  No reference counterpart. */
+gb_status gb_debug_hessenberg(gb_solver* s, double* h);
+
 /* number of kernels this library has launched (process-wide) */
 long long gb_launch_count(void);
 

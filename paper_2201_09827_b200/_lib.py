@@ -29,6 +29,7 @@ EXPORTS = [
     "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
     "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog", "gb_time_op",
+    "gb_debug_hessenberg",
 ]
 
 
@@ -102,6 +103,7 @@ def load(path: str | None = None):
         "gb_last_step_ms": (C.c_double, [vp]),
         "gb_debug_phaselog": (C.c_int, [vp, C.c_int, vp]),
         "gb_time_op": (C.c_int, [vp, C.c_int, C.c_int, dp]),
+        "gb_debug_hessenberg": (C.c_int, [vp, vp]),
         "gb_last_factor_ms": (C.c_double, [vp]),
         "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
                                        vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
@@ -276,6 +278,13 @@ class Solver:
             _check(self.lib.gb_debug_phaselog(self.h, cap, None), "gb_debug_phaselog")
         self._plog_cap = cap
         return out
+
+    def hessenberg(self) -> np.ndarray:
+        """(m+1) x m Hessenberg matrix of the last Arnoldi cycle (diagnostics)."""
+        m = self.opts.m
+        h = np.empty((m, m + 1))
+        _check(self.lib.gb_debug_hessenberg(self.h, _ptr(h)), "gb_debug_hessenberg")
+        return h.T.copy()
 
     @property
     def last_step_ms(self) -> float:

@@ -228,6 +228,13 @@ gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out) {
   return GB_OK;
 }
 
+gb_status gb_debug_hessenberg(gb_solver* s, double* h) {
+  if (!s || !h) return fail(GB_ERR_ARG, "null argument");
+  CK(cudaMemcpyAsync(h, s->H, sizeof(double) * (size_t)(s->o.m + 1) * s->o.m, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return GB_OK;
+}
+
 double gb_last_step_ms(gb_solver* s) { return s ? s->last_step_ms : 0.0; }
 double gb_last_factor_ms(gb_solver* s) { return s ? s->last_factor_ms : 0.0; }
 

@@ -19,6 +19,7 @@
 // exactly the reference's column sweep.
 #pragma once
 #include "gb_team.cuh"
+#include "gb_opseg.cuh"
 
 namespace gb {
 
@@ -165,6 +166,15 @@ struct SysView {
   const double* linv_lo;
   const double* uinv_hi;
   const double* uinv_lo;
+  // grid teams, fp64 operator (gb_opseg.cuh): inverses of the nbig x nbig
+  // diagonal blocks of L and U (row-major fp64 per block), the GEMV's bulk-copy
+  // stages and whether every entry of A is a normal number (integer-pipe
+  // conversion); bigl == nullptr -> the CTA-per-block substitution
+  const double* bigl = nullptr;
+  const double* bigu = nullptr;
+  int nbig = 0;
+  int gemv_ns = 0;
+  int a_normal = 0;
 };
 
 // progress counters of the flag-based TRSV (one per direction)
@@ -1170,6 +1180,31 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
   const int n = s.n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   mark(ts.log, 10);
+  if constexpr (Team::kGrid && Team::kTB == kTrsvB && M == MODE_F64) {
+    if (s.bigl != nullptr) {
+      // grid team, fp64 operator: bulk-copy GEMV + big-block substitutions
+      double* yb = reinterpret_cast<double*>(ybuf);
+      double* ysol = yb + s.lda;  // ybuf holds 2 ldv doubles
+      if (v != nullptr) {
+        if (s.a_normal)
+          seg::gemv_perm<TA, TV, true>(t, n, s.A, s.lda, s.perm, v, yb, smem, s.gemv_ns);
+        else
+          seg::gemv_perm<TA, TV, false>(t, n, s.A, s.lda, s.perm, v, yb, smem, s.gemv_ns);
+      } else {
+        int lo, hi;
+        t.rows(n, lo, hi);
+        for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) yb[i] = to_d(rvec[s.perm[i]]);
+      }
+      t.sync();
+      mark(ts.log, 11);
+      seg::sweep_bsp<TF, true>(t, n, s.nbig, s.LU, s.ldf, s.bigl, yb, ysol, seg::OutNone{}, smem);
+      mark(ts.log, 12);
+      seg::sweep_bsp<TF, false>(t, n, s.nbig, s.LU, s.ldf, s.bigu, ysol, yb, seg::OutTo<TW>{w}, smem);
+      mark(ts.log, 13);
+      ts.epoch++;
+      return;
+    }
+  }
   // 1. right-hand side in permuted order over the team's row slices
   int lo, hi;
   t.rows(n, lo, hi);

@@ -385,11 +385,15 @@ __global__ void k_set_system(const double* __restrict__ a, int n, TW* A, size_t 
   double rowmax = 0.0, bmax = 0.0;
   for (int i = warp; i < n; i += nwarps) {
     double s = 0.0;
+    bool odd = false;
     for (int j = lane; j < n; j += 32) {
       TW v = (TW)a[(size_t)i * n + j];
       A[(size_t)i * lda + j] = v;
       s += fabs((double)v);
+      const double av = fabs((double)v);
+      odd |= !(av >= (sizeof(TW) == 4 ? 1.1754943508222875e-38 : 2.2250738585072014e-308) && av <= 1.7976931348623157e308);
     }
+    if (__any_sync(0xffffffffu, odd) && lane == 0) atomicOr(&norms[2], 1ull);
     s = warp_sum(s);
     rowmax = (s > rowmax || s != s) ? s : rowmax;
     if (lane == 0) {
@@ -778,6 +782,10 @@ struct gb_solver {
   double *rcph = nullptr, *rcpl = nullptr, *xrcph = nullptr, *xrcpl = nullptr;
   double *linvh = nullptr, *linvl = nullptr, *uinvh = nullptr, *uinvl = nullptr;
   double *xlinvh = nullptr, *xlinvl = nullptr, *xuinvh = nullptr, *xuinvl = nullptr;
+  // grid teams with an fp64 operator: inverses of the big diagonal blocks
+  // (gb_opseg.cuh sweep_bsp), GEMV bulk-copy stages, A entries all normal
+  double *bigl = nullptr, *bigu = nullptr;
+  int nbig = 0, gemv_ns = 0, a_normal = 0;
   PivKey* lu_ckey = nullptr;
   double *lu_crow = nullptr, *lu_rowk = nullptr;
   int* lu_piv = nullptr;
@@ -851,6 +859,13 @@ struct Impl {
     K.recycling = (s->o.method == GB_RGMRES_IR || s->o.method == GB_RSGMRES_IR);
     K.sys = SysView<TW, TF>{s->n,     (size_t)s->lda, (const TW*)s->A, (size_t)s->lda, (const TF*)s->LU, s->perm,
                             s->rcph,  s->rcpl,        s->linvh,        s->linvl,        s->uinvh,          s->uinvl};
+    if (s->bigl != nullptr && s->gemv_ns > 0) {
+      K.sys.bigl = s->bigl;
+      K.sys.bigu = s->bigu;
+      K.sys.nbig = s->nbig;
+      K.sys.gemv_ns = s->gemv_ns;
+      K.sys.a_normal = s->a_normal;
+    }
     K.V = (TW*)s->V;
     K.w = (TW*)s->w;
     K.x = (TW*)s->xk;
@@ -936,6 +951,12 @@ struct Impl {
   static int trsv_block(const gb_solver* s) { return (s->G > 1 && !s->cluster) ? kTrsvB : 32; }
   static size_t smem_bytes(gb_solver* s) {
     size_t b = smem_bytes_for(s->o.m, s->o.k);
+    if (s->bigl != nullptr && s->gemv_ns > 0) {
+      // bulk-copy GEMV (v as fp64 + a ring filling the rest of 227 KB) and the
+      // big-block substitution's staged vector (sweep_bsp)
+      const size_t base = sm_doubles(s->o.m, s->o.k) * sizeof(double);
+      b = std::max(b, base + std::max(seg::gemv_smem(s->n, s->gemv_ns), (size_t)s->nbig * 8 + 64));
+    }
     if (trsv_block(s) == kTrsvB) {
       const size_t need = sm_doubles(s->o.m, s->o.k) * sizeof(double) +
                           std::max(trsv_cta_smem<MV, kTrsvB>(), trsv_cta_smem<MODE_F64, kTrsvB>());
@@ -1007,6 +1028,7 @@ struct Impl {
     if (st != GB_OK) return st;
     count_launch();
     void* argv[] = {(void*)&args...};
+    CK(cudaMemsetAsync(&s->ctl->count, 0, sizeof(unsigned), s->stream));  // GridTeam::sync arrival counter
     CK(cudaLaunchCooperativeKernel((void*)kern, dim3(s->G), dim3(kThreads), argv, sm, s->stream));
     return GB_OK;
   }
@@ -1036,6 +1058,12 @@ struct Impl {
       s->xlinvl = a.take<double>(ninv);
       s->xuinvh = a.take<double>(ninv);
       s->xuinvl = a.take<double>(ninv);
+      if (s->G > 1 && !s->cluster && MV == MODE_F64) {
+        s->nbig = n >= 8192 ? 2048 : 1024;
+        const size_t nk = (size_t)((n + s->nbig - 1) / s->nbig);
+        s->bigl = a.take<double>(nk * s->nbig * s->nbig);
+        s->bigu = a.take<double>(nk * s->nbig * s->nbig);
+      }
       s->lu_ckey = a.take<PivKey>(2 * 160);
       s->lu_crow = a.take<double>(2 * 160 * 32);
       s->lu_rowk = a.take<double>(64);
@@ -1073,7 +1101,7 @@ struct Impl {
       s->ctr = a.take<unsigned long long>(4);
       s->epoch = a.take<unsigned long long>(2);
       s->ytag = a.take<uint4>(2 * (size_t)ldv);
-      s->norms = a.take<unsigned long long>(2);
+      s->norms = a.take<unsigned long long>(4);
       s->ctl = a.take<GridCtl>(1);
       s->partials = a.take<double>((size_t)2 * s->G * s->kmax);
       s->cycle_iters = a.take<int>(m * 0 + s->o.max_cycles + 4);
@@ -1103,6 +1131,10 @@ struct Impl {
     s->mem_bytes = bytes;
     a.base = (char*)s->mem;
     plan(true);
+    if (s->bigl != nullptr) {
+      const size_t budget = 227 * 1024 - sm_doubles(s->o.m, s->o.k) * sizeof(double) - 1024;
+      s->gemv_ns = (budget > seg::gemv_vbytes(n) + 4608 + 2 * seg::GCH) ? seg::gemv_stages(n, budget) : 0;
+    }
     CK(cudaMemsetAsync(s->mem, 0, bytes, s->stream));
     return GB_OK;
   }
@@ -1118,16 +1150,17 @@ struct Impl {
       asrc = s->stage;
       bsrc = bstage;
     }
-    CK(cudaMemsetAsync(s->norms, 0, 2 * sizeof(unsigned long long), s->stream));
+    CK(cudaMemsetAsync(s->norms, 0, 3 * sizeof(unsigned long long), s->stream));
     int blocks = std::min(1184, std::max(1, (n + 7) / 8));
     count_launch();
     k_set_system<TW><<<blocks, 256, 0, s->stream>>>(asrc, n, (TW*)s->A, s->lda, bsrc, (TW*)s->b, s->norms);
     CK(cudaGetLastError());
-    unsigned long long nb[2];
+    unsigned long long nb[3];
     CK(cudaMemcpyAsync(nb, s->norms, sizeof(nb), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     memcpy(&s->normA, &nb[0], 8);
     memcpy(&s->normB, &nb[1], 8);
+    s->a_normal = nb[2] == 0 ? 1 : 0;  // no zero / subnormal / inf / NaN entry in fl_u(A)
     // fresh recycle state / counters for a new system
     CK(cudaMemsetAsync(s->keff_io, 0, 4 * sizeof(int), s->stream));
     s->parity = 0;
@@ -1137,9 +1170,20 @@ struct Impl {
   template <int M, class TA, class S>
   static gb_status lu_run(gb_solver* s, const TA* A, size_t lda, S* W, int* perm, int* piv, LuStatus* st,
                           double* rh, double* rl, double* ilh, double* ill, double* iuh, double* iul,
-                          int tcmode = 0) {
+                          int tcmode = 0, bool big = false) {
     gb_status e = lu_run_core<M>(s, A, lda, W, perm, piv, st, tcmode);
     if (e != GB_OK) return e;
+    if (big && s->bigl != nullptr) {
+      // inverses of the big diagonal blocks for the grid-team fp64 operator
+      const size_t smb = (size_t)8 * s->nbig * sizeof(double);
+      gb_status e2 = set_smem(seg::k_bigblock_inverse<S, true>, smb);
+      if (e2 == GB_OK) e2 = set_smem(seg::k_bigblock_inverse<S, false>, smb);
+      if (e2 != GB_OK) return e2;
+      count_launch(2);
+      seg::k_bigblock_inverse<S, true><<<148 * 4, 256, smb, s->stream>>>(W, (size_t)s->lda, s->n, s->nbig, s->bigl);
+      seg::k_bigblock_inverse<S, false><<<148 * 4, 256, smb, s->stream>>>(W, (size_t)s->lda, s->n, s->nbig, s->bigu);
+      CK(cudaGetLastError());
+    }
     count_launch(2);
     k_lu_rcp<S><<<std::max(1, std::min(1184, (s->n + 255) / 256)), 256, 0, s->stream>>>(W, s->lda, s->n, rh, rl);
     if (trsv_block(s) == kTrsvB) {
@@ -1198,6 +1242,7 @@ struct Impl {
       double* part = s->partials;
       void* argv[] = {(void*)&A,  (void*)&lda, (void*)&W,   (void*)&ldw,  (void*)&n,     (void*)&perm,
                       (void*)&st, (void*)&wk,  (void*)&ctl, (void*)&part, (void*)&tcmode};
+      CK(cudaMemsetAsync(&s->ctl->count, 0, sizeof(unsigned), s->stream));  // GridTeam::sync arrival counter
       CK(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(256), argv, smb, s->stream));
     }
     (void)piv;
@@ -1207,7 +1252,7 @@ struct Impl {
   static gb_status factor(gb_solver* s, int* zero_col, double* growth) {
     CK(cudaEventRecord(s->ev0, s->stream));
     gb_status e = lu_run<UM>(s, (const TW*)s->A, (size_t)s->lda, (typename LuT<UM>::S*)s->LU, s->perm, s->piv, s->lust,
-                             s->rcph, s->rcpl, s->linvh, s->linvl, s->uinvh, s->uinvl, s->o.lu_mode);
+                             s->rcph, s->rcpl, s->linvh, s->linvl, s->uinvh, s->uinvl, s->o.lu_mode, true);
     if (e != GB_OK) return e;
     CK(cudaEventRecord(s->ev1, s->stream));
     LuStatus h;

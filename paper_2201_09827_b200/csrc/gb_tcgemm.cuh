@@ -1,0 +1,245 @@
+// Tensor-core trailing update of the blocked fp16 LU (tensor mode, SURVEY
+// §8(a) a6, densela.py:148-168 restated as a blocked GEPP):
+//
+//   C <- fl16( C - fp32( A * Bt^T ) )      A = L21 (M x K), Bt = U12^T (N x K)
+//
+// with K = the panel width (a multiple of 32).  One persistent,
+// warp-specialised kernel per panel:
+//   warp 0  TMA producer: 2-D tensor-map loads (SWIZZLE_64B, K-major 32-wide
+//           slabs) of A (128 x 32) and Bt (256 x 32) into an STAGES-deep
+//           ring of shared-memory stages, one mbarrier (expect_tx) per stage;
+//   warp 1  MMA issuer: one thread issues tcgen05.mma kind::f16 (128 x 256 x
+//           16, fp32 accumulator in TMEM), tcgen05.commit frees the stage;
+//   warp 2  TMEM allocator (512 columns = two 128 x 256 fp32 accumulators);
+//   warps 4-7  epilogue: tcgen05.ld of the accumulator (warp 4+q reads TMEM
+//           lanes 32q..32q+31 = rows of the tile), C read, fl16(C - acc),
+//           store; the accumulator buffer is handed back through an mbarrier,
+//           so the epilogue of tile t overlaps the MMAs of tile t+1.
+// Tiles (128 x 256 of C) are dealt round-robin over the persistent CTAs.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gb_tc.cuh"
+
+namespace gb {
+namespace tcg {
+
+constexpr int BM = 128, BN = 256, BK = 32;        // tile and K slab (64-byte K-major rows)
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;              // 8 KB
+constexpr int B_BYTES = BN * BK * 2;              // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;    // 24 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;  // + alignment + barriers
+constexpr int NTHREADS = 256;
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// C rows [r0, r0 + M), columns [c0, c0 + N) of W (row-major, leading dim ld);
+// A via map_a at (column k0, row r0 + ...), Bt via map_b (row = C column - c0)
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_tc_update(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, __half* W,
+                size_t ld, int r0, int c0, int M, int N, int k0, int K) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  const int ntiles = tm * tn;
+  const int nslab = K / BK;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      tc::mbar_init(full + i, 1);
+      tc::mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(tfull + i, 1);
+      tc::mbar_init(tempty + i, 4);  // one elected arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&map_a);
+    prefetch_map(&map_b);
+  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    int st = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int ti = t / tn, tj = t % tn;
+      for (int s = 0; s < nslab; ++s) {
+        tc::mbar_wait(empty + st, ph ^ 1u);
+        unsigned char* sa = smem + st * STAGE_BYTES;
+        unsigned char* sb = sa + A_BYTES;
+        mbar_expect_tx(full + st, STAGE_BYTES);
+        tma_2d(sa, &map_a, k0 + s * BK, r0 + ti * BM, full + st);
+        tma_2d(sb, &map_b, s * BK, tj * BN, full + st);
+        if (++st == STAGES) st = 0, ph ^= 1u;
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (single thread)
+    constexpr uint32_t idesc = tc::idesc_f16_f32(BM, BN);
+    int st = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t aph = (uint32_t)((it >> 1) & 1);
+      tc::mbar_wait(tempty + acc, aph ^ 1u);  // the epilogue drained this accumulator
+      tc::fence_after();
+      const uint32_t dt = tmem + (uint32_t)(acc * BN);
+      for (int s = 0; s < nslab; ++s) {
+        tc::mbar_wait(full + st, ph);
+        tc::fence_after();
+        const unsigned char* sa = smem + st * STAGE_BYTES;
+        const uint64_t ad = tc::desc_k64(tc::smem_u32(sa)), bd = tc::desc_k64(tc::smem_u32(sa + A_BYTES));
+        tc::mma_f16(dt, ad, bd, idesc, s > 0 ? 1u : 0u);
+        tc::mma_f16(dt, ad + 2, bd + 2, idesc, 1u);  // K = 16..31: +32 bytes inside the swizzle atom
+        tc::commit(empty + st);                       // frees the stage once these MMAs completed
+        if (++st == STAGES) st = 0, ph ^= 1u;
+      }
+      tc::commit(tfull + acc);  // accumulator complete
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: row = TMEM lane
+    const int q = warp - 4;
+    const int row_in_tile = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int ti = t / tn, tj = t % tn;
+      const int acc = it & 1;
+      tc::mbar_wait(tfull + acc, (uint32_t)((it >> 1) & 1));
+      tc::fence_after();
+      const int gi = ti * BM + row_in_tile;  // row inside the update
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tc::tmem_ld32(tbase + (uint32_t)(ch * 32), v);
+        const int gj = tj * BN + ch * 32;
+        if (gi < M && gj < N) {
+          __half* p = W + (size_t)(r0 + gi) * ld + c0 + gj;
+          if (gj + 32 <= N) {
+            __align__(16) __half h[32];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) reinterpret_cast<uint4*>(h)[z] = reinterpret_cast<const uint4*>(p)[z];
+#pragma unroll
+            for (int z = 0; z < 32; ++z) h[z] = __float2half_rn(__half2float(h[z]) - v[z]);
+#pragma unroll
+            for (int z = 0; z < 4; ++z) reinterpret_cast<uint4*>(p)[z] = reinterpret_cast<const uint4*>(h)[z];
+          } else {
+            for (int z = 0; z < 32 && gj + z < N; ++z) p[z] = __float2half_rn(__half2float(p[z]) - v[z]);
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) tc::tmem_dealloc(tmem, 512);
+}
+
+// Bt[j][k] = U12[k][j] (K x N of W at rows [k0, k0 + K), columns [c0, c0 + N))
+// into the K-major scratch (row stride K)
+__global__ void k_transpose_u12(const __half* __restrict__ W, size_t ld, int k0, int c0, int K, int N,
+                                __half* __restrict__ Bt) {
+  __shared__ __half tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx: column (N), by: row (K)
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = by + i, j = bx + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && j < N) ? W[(size_t)(k0 + k) * ld + c0 + j] : __float2half(0.f);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int j = bx + i, k = by + threadIdx.x;
+    if (j < N && k < K) Bt[(size_t)j * K + k] = tile[threadIdx.x][i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: tensor maps through the driver entry point (no libcuda link needed)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp16 map over a row-major matrix (rows x cols, row pitch in elements),
+// box = box_rows x 32 columns, SWIZZLE_64B (the UMMA K-major SW64 atom)
+inline bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                     uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {pitch_elems * 2};
+  const cuuint32_t box[2] = {BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// W[r0:r0+M, c0:c0+N] -= W[r0:r0+M, k0:k0+K] * W[k0:k0+K, c0:c0+N]  (fp32
+// accumulation, one fl16 rounding); Bt: scratch of N * K halves
+inline cudaError_t tc_update(__half* W, size_t ld, int nrows, int r0, int c0, int M, int N, int k0, int K,
+                             __half* Bt, int nsm, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  dim3 tb(32, 8), tg((N + 31) / 32, (K + 31) / 32);
+  k_transpose_u12<<<tg, tb, 0, st>>>(W, ld, k0, c0, K, N, Bt);
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, W, (uint64_t)nrows, ld, ld, BM) || !make_map(&mb, Bt, (uint64_t)N, (uint64_t)K, K, BN))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tc_update, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  k_tc_update<<<ntiles < nsm ? ntiles : nsm, NTHREADS, SMEM_BYTES, st>>>(ma, mb, W, ld, r0, c0, M, N, k0, K);
+  return cudaGetLastError();
+}
+
+}  // namespace tcg
+}  // namespace gb

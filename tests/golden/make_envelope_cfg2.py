@@ -43,6 +43,8 @@ VARIANTS = {
     "reversed": (True, False, "reversed"),
     "wide": (True, False, "wide"),
     **{f"ulp{s}": (False, False, f"ulp{s}") for s in range(8)},
+    # unblocked fp32 LU together with a last-bit move of the first update
+    **{f"lu_ulp{s}": (False, True, f"ulp{s}") for s in range(4)},
 }
 
 

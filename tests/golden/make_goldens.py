@@ -405,6 +405,86 @@ def case_variants():
 CASES["variants"] = case_variants
 
 
+# well-posed recycling systems in the cluster-team range n in (256, 1024]
+# (VERDICT r1 item 1 / SURVEY F7): cold cycle >= k, deflated cycles, warm
+# starts in later refinement steps, converging
+WELLPOSED = [
+    # (tag, n, kappa, seed, precisions, m, k, tau)
+    ("w1024_hsd", 1024, 1e3, 3, ("half", "single", "double"), 10, 4, 1e-4),
+    ("w1024_hdq", 1024, 1e3, 3, ("half", "double", "quad"), 10, 4, 1e-6),
+    ("w1024_sdq", 1024, 1e7, 3, ("single", "double", "quad"), 10, 4, 1e-10),
+]
+
+
+def case_wellposed():
+    out = {}
+    for tag, n, kappa, seed, prec, m, k, tau in WELLPOSED:
+        a = problems.randsvd(n, kappa, seed)
+        b = problems.rhs_normal(n, seed)
+        d = _solve(a, b, prec, "rgmres-ir", m, k, tau, 10)
+        d.update(n=n, kappa=kappa, seed=seed, a_sha=_sha(a), b_sha=_sha(b))
+        out[tag] = d
+        print(tag, d["inner_iters"], d["converged"], [c["cycles"] for c in d["inner_calls"]], flush=True)
+    _dump("wellposed", out)
+
+
+CASES["wellposed"] = case_wellposed
+
+
+def _first_divergence_unblocked(a_u, ref_perm):
+    """First step where an unblocked, FMA-free fp32 GEPP of the same matrix
+    picks a different pivot row than the reference's sgetrf (None if never)."""
+    w = a_u.astype(np.float32)
+    n = w.shape[0]
+    perm = np.arange(n)
+    for k in range(n):
+        p = k + int(np.argmax(np.abs(w[k:, k])))
+        if p != k:
+            w[[k, p], :] = w[[p, k], :]
+            perm[[k, p]] = perm[[p, k]]
+        if perm[k] != ref_perm[k]:
+            return k
+        if w[k, k] != 0:
+            w[k + 1:, k] *= np.float32(1) / w[k, k]
+            w[k + 1:, k + 1:] -= np.outer(w[k + 1:, k], w[k, k + 1:])
+    return None
+
+
+def case_lu_large():
+    """Pivot goldens beyond n = 1024: exact fp16 GEPP at n = 2048 (randsvd
+    kappa 1e8, the config-5 analogue with fp16 subnormals) and the
+    fp32 sgetrf pivots of config 4 (n = 8192).  For the fp32 cases the first
+    pivot where another valid GEPP of the same matrix (unblocked, no FMA)
+    departs from the reference is recorded too: the parity noise floor
+    (SURVEY F14)."""
+    meta, arrays = {}, {}
+    H, S_, D = precision.Format.HALF, precision.Format.SINGLE, precision.Format.DOUBLE
+    a = problems.randsvd(2048, 1e8, 1)
+    a_u = precision.round_array(a, S_)
+    t0 = time.perf_counter()
+    f, packed = _lu_record(a_u, H)
+    arrays["r2048k8_half_perm"] = f.perm.astype(np.int64)
+    arrays["r2048k8_half_diag"] = np.diag(packed).copy()
+    arrays["r2048k8_half_row7"] = packed[7].copy()
+    meta["r2048k8_half"] = {"n": 2048, "u": "single", "uf": "half", "growth": f.growth, "lu_sha": _sha(packed),
+                            "a_sha": _sha(a), "seconds": time.perf_counter() - t0}
+    print("r2048k8_half", meta["r2048k8_half"], flush=True)
+    for name, a in (("cfg2a_single", problems.prolate(1024, 0.45)),
+                    ("cfg4_single", problems.randsvd(8192, 1e6, 1))):
+        a_u = precision.round_array(a, D)
+        f, packed = _lu_record(a_u, S_)
+        alt = _first_divergence_unblocked(a_u, f.perm)
+        arrays[f"{name}_perm"] = f.perm.astype(np.int64)
+        arrays[f"{name}_diag"] = np.diag(packed).copy()
+        meta[name] = {"n": int(a.shape[0]), "u": "double", "uf": "single", "growth": f.growth,
+                      "a_sha": _sha(a), "alt_divergence": alt}
+        print(name, meta[name], flush=True)
+    _dump("lu_large", meta, arrays)
+
+
+CASES["lu_large"] = case_lu_large
+
+
 if __name__ == "__main__":
     if os.environ.get("OPENBLAS_NUM_THREADS") != "1":
         sys.exit("set OPENBLAS_NUM_THREADS=1 (SURVEY.md F14)")

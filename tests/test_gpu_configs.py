@@ -1,0 +1,365 @@
+"""Solver parity on the BASELINE configurations the bench runs, against runs of
+the reference itself (tests/golden/make_goldens.py):
+
+* config 2 (prolate n=1024, both u_f) on the cluster-team kernel type: the
+  reference stagnates at the 205-cycle cap.  Per-cycle Arnoldi
+  steps and k_eff are compared cycle by cycle (the first divergence is
+  reported), and the Arnoldi total must lie in the reference's own
+  perturbation envelope (tests/golden/cfg2_envelope.json, make_envelope_cfg2.py);
+* well-posed recycling systems in the same n range (cold + deflated cycles,
+  warm starts, converging): per-step counts within +-1;
+* config 4 (randsvd n=8192, single/double/quad, both methods);
+* the config-5 analogue at n=1024 (fp16 LU at kappa 1e8, x0 reset,
+  InnerStagnation at the cycle cap);
+* large-n LU pivots: exact fp16 at n=2048 (bit-identical), fp32 at n=1024 and
+  8192 (identical up to the reference's own noise floor);
+* the forward-error reference solution xref (both recipes) and the
+  S-variant operator at u.
+"""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_json, golden_npz
+from oracle import cpu_gcrodr_ir as O
+from paper_2201_09827_b200 import _lib, problems
+from paper_2201_09827_b200.precision import Format, PrecisionTriple
+from paper_2201_09827_b200.refine import DivergenceReason, Method, RefineConfig, _refine, make_options
+from test_gpu_solve import _level_ok
+
+pytestmark = pytest.mark.gpu
+
+
+def _sha(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _cfg(spec_prec, method, m, k, tau, i_max, **kw):
+    return RefineConfig(PrecisionTriple.parse(*spec_prec), Method.parse(method), m=m,
+                        k=k if method.startswith("r") else 0, tau=tau, i_max=i_max, **kw)
+
+
+def first_cycle_divergence(ours_c, ours_k, ref_c, ref_k):
+    for i, (a, b, c, d) in enumerate(zip(ours_c, ref_c, ours_k, ref_k)):
+        if a != b or c != d:
+            return i
+    return min(len(ours_c), len(ref_c))
+
+
+# ---------------------------------------------------------------------------
+# config 2
+# ---------------------------------------------------------------------------
+
+def _envelope(cfg):
+    p = os.path.join(GOLDEN, "cfg2_envelope.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(cfg)
+
+
+@pytest.mark.parametrize("name", ["cfg2a", "cfg2b"])
+def test_config2_cluster_team(gpu, name):
+    spec = problems.CONFIGS[name]
+    g = golden_json(name)["rgmres-ir"]
+    a, b = problems.config_problem(spec)
+    assert _sha(a) == golden_json(name)["a_sha"] and _sha(b) == golden_json(name)["b_sha"]
+    trace = []
+    rep = _refine(a, b, _cfg(spec.precisions, "rgmres-ir", spec.m, spec.k, spec.tau, spec.i_max), trace=trace)
+    # same verdict: stagnation of the inner solve at the cycle cap in step 1
+    assert not rep.converged and rep.divergence_reason is DivergenceReason.INNER_STAGNATION, rep
+    assert rep.steps == g["steps"] == 1
+    call = g["inner_calls"][0]
+    ours_c, ours_k = trace[0]["cycles"], trace[0]["k_eff"]
+    assert len(ours_c) == len(call["cycles"]) == 205  # ceil(10 n / m) cycles, cold + 204 deflated
+    first = first_cycle_divergence(ours_c, ours_k, call["cycles"], call["k_eff"])
+    print(f"{name}: per-cycle (steps, k_eff) identical to the reference for the first {first} of 205 cycles; "
+          f"total {rep.inner_iters[0]} vs {g['inner_iters'][0]}")
+    if spec.precisions[0] == "half":
+        # exact fp16 LU: identical factors and x0, so the cold cycle, its
+        # harvest and the first deflated cycles agree exactly.  (cfg2a's fp32
+        # LU of this numerically singular matrix differs from OpenBLAS sgetrf
+        # in the last bits, and x0 -- an O(1e17) vector of rounding noise --
+        # with it: there only the total is comparable, against the envelope.)
+        assert first >= 2, (ours_c[:8], call["cycles"][:8], ours_k[:8], call["k_eff"][:8])
+    # every deflated cycle but the last is m - k_eff(previous) steps: recycling
+    # kept k or k+1 vectors (the last may stop early on a non-finite iterate)
+    for c, kp in zip(ours_c[1:-1], ours_k[:-2]):
+        assert c == spec.m - kp
+    env = _envelope(name)
+    if env is None:
+        pytest.skip("tests/golden/cfg2_envelope.json not generated (tests/golden/make_envelope_cfg2.py)")
+    tot = rep.inner_iters[0]
+    assert env["lo"] - 1 <= tot <= env["hi"] + 1, (tot, env["lo"], env["hi"])
+
+
+# ---------------------------------------------------------------------------
+# well-posed recycling systems, cluster team
+# ---------------------------------------------------------------------------
+
+def _wellposed():
+    p = os.path.join(GOLDEN, "wellposed.json")
+    if not os.path.exists(p):
+        return []
+    d = json.load(open(p))
+    return [(k, v) for k, v in sorted(d.items()) if not k.startswith("_")]
+
+
+@pytest.mark.parametrize("tag,g", _wellposed(), ids=lambda x: x if isinstance(x, str) else "")
+def test_wellposed_recycling(gpu, tag, g):
+    n, seed = g["n"], g["seed"]
+    a = problems.randsvd(n, g["kappa"], seed)
+    b = problems.rhs_normal(n, seed)
+    assert _sha(a) == g["a_sha"]
+    trace = []
+    rep = _refine(a, b, _cfg(g["precisions"], "rgmres-ir", g["m"], g["k"], g["tau"], g["i_max"]), trace=trace)
+    assert rep.converged == g["converged"] and rep.converged, (rep.inner_iters, g["inner_iters"])
+    assert rep.steps == g["steps"], (rep.inner_iters, g["inner_iters"])
+    for ours, ref in zip(rep.inner_iters, g["inner_iters"]):
+        assert abs(ours - ref) <= 1, (rep.inner_iters, g["inner_iters"], trace)
+    # recycling is exercised: deflated cycles in step 1, a warm start later
+    calls = g["inner_calls"]
+    assert "deflated" in calls[0]["cycle_kind"] and any(c["warm"] for c in calls[1:])
+    if g["precisions"][0] == "half":
+        # exact fp16 LU (bit-identical factors and x0): the cold cycle and its
+        # harmonic-Ritz harvest are reproduced exactly.  With fp32 factors the
+        # LU differs from OpenBLAS sgetrf in the last bits, x0
+        # with it, and per-cycle counts are only compared through the totals
+        first = first_cycle_divergence(trace[0]["cycles"], trace[0]["k_eff"], calls[0]["cycles"], calls[0]["k_eff"])
+        assert first >= 1, (trace[0], calls[0])
+    u = 2.0 ** -24 if g["precisions"][1] == "single" else 2.0 ** -53
+    floor = 2.0 * u
+    assert _level_ok(rep.nbe_final, g["nbe_history"][-1], 10.0, floor * 0.05)
+    assert _level_ok(rep.ferr_final, g["ferr_history"][-1], 10.0, floor * 0.05)
+
+
+# ---------------------------------------------------------------------------
+# config 4 (n = 8192, grid team, dd operator and residual)
+# ---------------------------------------------------------------------------
+
+_CFG4 = {}
+
+
+def _cfg4_inputs():
+    if "ab" not in _CFG4:
+        from threadpoolctl import threadpool_limits
+
+        g = golden_json("cfg4")
+        with threadpool_limits(1):  # the golden's A was generated single-threaded
+            a, b = problems.config_problem(problems.CONFIGS["cfg4"])
+        _CFG4["ab"] = (a, b, _sha(a) == g["a_sha"] and _sha(b) == g["b_sha"])
+    return _CFG4["ab"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("method", ["rgmres-ir", "gmres-ir"])
+def test_config4(gpu, method):
+    spec = problems.CONFIGS["cfg4"]
+    g = golden_json("cfg4")[method]
+    a, b, same = _cfg4_inputs()
+    assert same, "config-4 input differs from the reference's (BLAS build?)"
+    rep = _refine(a, b, _cfg(spec.precisions, method, spec.m, spec.k, spec.tau, spec.i_max))
+    assert rep.converged and g["converged"]
+    assert rep.steps == g["steps"], (rep.inner_iters, g["inner_iters"])
+    for ours, ref in zip(rep.inner_iters, g["inner_iters"]):
+        assert abs(ours - ref) <= 1, (rep.inner_iters, g["inner_iters"])
+    floor = 2.0 * 2.0 ** -53
+    assert _level_ok(rep.nbe_final, g["nbe_history"][-1], 10.0, floor * 0.05), (rep.nbe_history, g["nbe_history"])
+    assert _level_ok(rep.ferr_final, g["ferr_history"][-1], 10.0, floor * 0.05), (rep.ferr_history, g["ferr_history"])
+    assert abs(np.max(np.abs(rep.solution)) - g["solution_inf"]) <= 1e-12 * g["solution_inf"]
+
+
+# ---------------------------------------------------------------------------
+# config-5 analogue (n = 1024): fp16 LU at kappa 1e8, x0 overflow -> reset
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("method", ["gmres-ir", "rgmres-ir"])
+def test_config5_analogue(gpu, method):
+    spec = problems.CONFIGS["cfg5"]
+    G = golden_json("cfg5_1024")
+    g = G[method]
+    a, b = problems.config_problem(spec, 0, 1024)
+    assert _sha(a) == G["a_sha"]
+    trace = []
+    rep = _refine(a, b, _cfg(spec.precisions, method, spec.m, spec.k, spec.tau, spec.i_max), trace=trace)
+    assert rep.diagnostics.get("x0_reset") and g["diagnostics"].get("x0_reset")
+    assert not rep.converged and rep.divergence_reason is DivergenceReason.INNER_STAGNATION
+    assert rep.steps == g["steps"] == 1
+    call = g["inner_calls"][0]
+    assert len(trace[0]["cycles"]) == len(call["cycles"]) == 52  # ceil(10 * 1024 / 200)
+    if method == "gmres-ir":
+        assert rep.inner_iters == g["inner_iters"] == [10400]
+    else:
+        first = first_cycle_divergence(trace[0]["cycles"], trace[0]["k_eff"], call["cycles"], call["k_eff"])
+        print(f"cfg5_1024 rgmres-ir: per-cycle identical for {first} of 52 cycles; total {rep.inner_iters} vs "
+              f"{g['inner_iters']}")
+        assert first >= 2
+        # each deflated cycle is m - k_eff steps with k_eff in {k, k+1}: the
+        # total can only move by the number of conjugate-pair straddles
+        assert abs(rep.inner_iters[0] - g["inner_iters"][0]) <= 52
+    assert _level_ok(rep.nbe_final, g["nbe_history"][-1], 10.0)
+    assert _level_ok(rep.ferr_final, g["ferr_history"][-1], 10.0)
+
+
+# ---------------------------------------------------------------------------
+# LU pivots at larger n
+# ---------------------------------------------------------------------------
+
+def _solver(a, uf, u, ur="double", n=None):
+    n = a.shape[0]
+    cfg = RefineConfig(PrecisionTriple.parse(uf, u, ur), method=Method.GMRES_IR, m=min(n, 20))
+    s = _lib.Solver(n, make_options(cfg, n))
+    s.set_system(a, np.ones(n))
+    return s
+
+
+def test_lu_half_kappa1e8_n1024(gpu):
+    """fp16 exact GEPP on the config-5 analogue matrix (randsvd 1024, kappa
+    1e8: fp16 subnormals): pivots and U diagonal bit-identical."""
+    z = golden_npz("lu")
+    meta = golden_json("lu")["r1024k8_half"]
+    s = _solver(problems.randsvd(1024, 1e8, 1), "half", "single")
+    zero, growth = s.factorize()
+    lu, perm = s.factors()
+    assert zero == -1 and growth == meta["growth"]
+    assert np.array_equal(perm, z["r1024k8_half_perm"])
+    assert np.array_equal(np.diag(lu), z["r1024k8_half_diag"])
+    s.close()
+
+
+def _lu_large():
+    p = os.path.join(GOLDEN, "lu_large.json")
+    return (json.load(open(p)), np.load(os.path.join(GOLDEN, "lu_large.npz"))) if os.path.exists(p) else (None, None)
+
+
+def test_lu_half_n2048(gpu):
+    meta, z = _lu_large()
+    if meta is None:
+        pytest.skip("lu_large golden not generated")
+    m = meta["r2048k8_half"]
+    a = problems.randsvd(2048, 1e8, 1)
+    assert _sha(a) == m["a_sha"]
+    s = _solver(a, "half", "single")
+    zero, growth = s.factorize()
+    lu, perm = s.factors()
+    assert zero == -1 and growth == m["growth"]
+    assert np.array_equal(perm, z["r2048k8_half_perm"])
+    assert np.array_equal(np.diag(lu), z["r2048k8_half_diag"])
+    assert np.array_equal(lu[7], z["r2048k8_half_row7"])
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2a_single", "cfg4_single"])
+def test_lu_single_pivots_large(gpu, name):
+    """fp32 LU (the reference's sgetrf): the pivot sequence equals
+    the reference's up to the step where another valid GEPP of the same
+    matrix (unblocked, FMA-free) also departs from it -- the reference's own
+    rounding-noise floor; reported either way."""
+    meta, z = _lu_large()
+    if meta is None:
+        pytest.skip("lu_large golden not generated")
+    m = meta[name]
+    if name == "cfg2a_single":
+        a = problems.prolate(1024, 0.45)
+    else:
+        a = _cfg4_inputs()[0]
+    assert _sha(a) == m["a_sha"]
+    s = _solver(a, "single", "double")
+    s.factorize()
+    lu, perm = s.factors()
+    s.close()
+    ref = z[f"{name}_perm"]
+    d = np.nonzero(perm != ref)[0]
+    first = int(d[0]) if d.size else None
+    alt = m["alt_divergence"]
+    print(f"{name}: first pivot difference at {first}; reference-vs-unblocked noise floor {alt}")
+    if first is not None and alt is not None:
+        assert first >= alt - 16, (first, alt)
+    elif first is not None:
+        pytest.fail(f"pivot {first} differs although an alternative GEPP agrees with the reference throughout")
+    # the factors reach the same quality (growth within 2x)
+    assert np.max(np.abs(np.diag(lu))) > 0 and abs(np.log2(np.max(np.abs(np.triu(lu))) /
+                                                           np.max(np.abs(np.float32(a))) / m["growth"])) < 1
+
+
+# ---------------------------------------------------------------------------
+# xref and the S-variant operator
+# ---------------------------------------------------------------------------
+
+def test_xref_dd_gepp(gpu):
+    """xref for n <= 600 is the double-double GEPP quad_solve
+    (densela.py:368-407): the same elementwise dd operation sequence, so it
+    matches the reference's xref to the last bit of the fp64 result."""
+    k = golden_npz("kernels")
+    a, b = k["a"], k["b"]
+    # the golden quad_solve ran on the unrounded fp64 system: u = double keeps it unrounded
+    cfg = RefineConfig(PrecisionTriple.parse("half", "double", "double"), method=Method.GMRES_IR, m=20)
+    s = _lib.Solver(100, make_options(cfg, 100))
+    s.set_system(a, b)
+    assert s.reference_solution()
+    x = s.reference()
+    ref = k["xref_q"]
+    np.testing.assert_allclose(x, ref, rtol=0, atol=2.0 ** -52 * np.max(np.abs(ref)))
+    s.close()
+
+
+def test_xref_lu_refinement_n1024(gpu):
+    """xref for n > 600: fp64 LU + 4 sweeps of dd-residual refinement
+    (refine.py:251-256), against the pinned oracle on the config-5 analogue
+    (kappa 1e8).  Both reach the dd-refined solution to fp64 accuracy."""
+    a, b = problems.config_problem(problems.CONFIGS["cfg5"], 0, 1024)
+    a_u, b_u = O.rnd(a, "single"), O.rnd(b, "single")
+    ref = O.reference_solution(a_u, b_u)
+    cfg = RefineConfig(PrecisionTriple.parse("half", "single", "double"), method=Method.GMRES_IR, m=20)
+    s = _lib.Solver(1024, make_options(cfg, 1024))
+    s.set_system(a, b)
+    assert s.reference_solution()
+    x = s.reference()
+    s.close()
+    err = np.max(np.abs(x - ref)) / np.max(np.abs(ref))
+    assert err <= 64 * 2.0 ** -53, err
+
+
+@pytest.mark.parametrize("tag,uf,u", [("hs", "half", "single"), ("hd", "half", "double")])
+def test_operator_at_u(gpu, tag, uf, u):
+    """apply_preconditioned at u (the S-variants' operator, refine.py:129-131)
+    for identical fp16 factors: within one rounding of u of the reference."""
+    k = golden_npz("kernels")
+    a, b = k["a"], k["b"]
+    # uniform-precision method: the device context runs the operator at u
+    cfg = RefineConfig(PrecisionTriple.parse(uf, u, "double"), method=Method.SGMRES_IR, m=20)
+    s = _lib.Solver(100, make_options(cfg, 100))
+    s.set_system(a, b)
+    s.factorize()
+    w = s.apply_preconditioned(k[f"{tag}_v"], Format.parse(u).code)
+    ref = k[f"{tag}_op_u"]
+    tol = 2.0 ** -23 if u == "single" else 2.0 ** -51
+    # the operator at u rounds after every elementary step; results agree to
+    # kappa-amplified roundings of u
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(w - ref)) <= 1e4 * tol * scale
+    s.close()
+
+
+# ---------------------------------------------------------------------------
+# options: reorthogonalize=False
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("method", ["gmres-ir", "rgmres-ir"])
+def test_no_reorthogonalization(gpu, method):
+    """reorthogonalize=False skips the selective second MGS pass
+    (gmres.py:173-178): per-step counts +-1 of the oracle in the same mode."""
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    for m, k in ((100, 5), (8, 3)):
+        cfg = _cfg(("half", "single", "double"), method, m, k, 1e-4, 10, reorthogonalize=False)
+        rep = _refine(a, b, cfg)
+        ref = O.solve(a, b, ("half", "single", "double"), method, m, k if method[0] == "r" else 0, 1e-4, 10,
+                      reorthogonalize=False)
+        assert rep.converged == ref.converged and rep.steps == ref.steps, (rep.inner_iters, ref.inner_iters)
+        assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters,
+                                                                                         ref.inner_iters)

@@ -1,0 +1,426 @@
+// Micro-benchmark of the segment-pipelined operator (csrc/gb_opseg.cuh):
+// w = fl32(U^-1 L^-1 (A v)[perm]) with fp16 factors, fp32 A, fp64 operator,
+// on a cooperative grid of 148 CTAs; checked against a host fp64 reference.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -I include tools/micro/opseg.cu -o tools/micro/opseg
+//   ./opseg [n] [reps]
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+#include <random>
+#include <algorithm>
+#include "../../paper_2201_09827_b200/csrc/gb_opseg.cuh"
+#ifndef NBIG
+#define NBIG 1024
+#endif
+
+using namespace gb;
+#ifndef KSEG
+#define KSEG 2
+#endif
+
+struct Out32 {
+  float* w;
+  __device__ void operator()(int i, double v) const { w[i] = __double2float_rn(v); }
+};
+struct OutNone {
+  __device__ void operator()(int, double) const {}
+};
+
+__global__ void __launch_bounds__(256, 1) k_op(int n, const float* A, size_t lda, const int* perm, const float* v,
+                                               const __half* LU, size_t ldf, const double* linv, const double* uinv,
+                                               double* t, uint4* tl, uint4* tu, uint4* pl, uint4* pu, float* w, GridCtl* ctl,
+                                               unsigned epoch, int phases, unsigned long long* stamps, int gstages, const double* dlbig, const double* dubig, double* ysc) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  GridTeam team;
+  team.G = gridDim.x;
+  team.r = blockIdx.x;
+  team.ctl = ctl;
+  team.partials = nullptr;
+  team.kmax = 0;
+  team.phase = 0;
+  unsigned long long t0 = 0;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0) t0 = gtimer();
+  if (phases & 1) {
+    seg::gemv_perm<float, float, true>(team, n, A, lda, perm, v, t, smem, gstages);
+    team.sync();
+  }
+  if (phases & 128) {
+    for (int i = 0; i < 1000; ++i) team.sync();
+  }
+  if (phases & 8) {
+    seg::gemv_ldg<float, float, 1, 16>(team, n, A, lda, perm, v, t, smem);
+    team.sync();
+  }
+  if (phases & 16) {
+    seg::gemv_ldg<float, float, 0, 16>(team, n, A, lda, perm, v, t, smem);
+    team.sync();
+  }
+  if (phases & 32) {
+    seg::gemv_ldg<float, float, 2, 16>(team, n, A, lda, perm, v, t, smem);
+    team.sync();
+  }
+  if (phases & 64) {
+    seg::gemv_ldg<float, float, 3, 16>(team, n, A, lda, perm, v, t, smem);
+    team.sync();
+  }
+  unsigned long long t1 = 0;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0) t1 = gtimer();
+  seg::SweepIO lo{n, LU, ldf, linv, t, nullptr, 0u, tl, 2 * epoch + 1, stamps ? stamps + 8 : nullptr};
+#if KSEG == -1
+  if (phases & 2) seg::sweep_bsp<__half, true>(team, n, NBIG, LU, ldf, dlbig, t, ysc, OutNone{}, smem);
+#elif KSEG == 0
+  if (phases & 2) seg::sweep2<__half, true>(team, seg::SweepIO2{lo, pl}, smem, OutNone{});
+#else
+  if (phases & 2) seg::sweep<__half, true, KSEG>(team, lo, smem, OutNone{});
+#endif
+  seg::SweepIO up{n, LU, ldf, uinv, nullptr, tl, 2 * epoch + 1, tu, 2 * epoch + 2, stamps ? stamps + 8 + 8 * 1024 : nullptr};
+#if KSEG == -1
+  if (phases & 4) seg::sweep_bsp<__half, false>(team, n, NBIG, LU, ldf, dubig, ysc, t, Out32{w}, smem);
+#elif KSEG == 0
+  if (phases & 4) seg::sweep2<__half, false>(team, seg::SweepIO2{up, pu}, smem, Out32{w});
+#else
+  if (phases & 4) seg::sweep<__half, false, KSEG>(team, up, smem, Out32{w});
+#endif
+  team.sync();
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+    stamps[0] = t1 - t0;
+    stamps[1] = gtimer() - t1;
+  }
+}
+
+__global__ void k_stream(const uint4* p, size_t nvec, double* out) {
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nvec; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 q;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(p + i));
+    acc += (double)(q.x ^ q.y ^ q.z ^ q.w);
+  }
+  if (acc == 1234.5) out[0] = acc;
+}
+
+// access-pattern probes (trivial compute): warp-per-row and CTA-per-row in perm order
+template <int U, bool kCtaRow>
+__global__ void __launch_bounds__(256, 1) k_rowstream(const uint4* A, size_t ldv, const int* perm, int n, int nv, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned acc = 0;
+  if (!kCtaRow) {
+    for (int i = blockIdx.x * 8 + wid; i < n; i += gridDim.x * 8) {
+      const uint4* row = A + (size_t)perm[i] * ldv;
+      for (int base = lane; base < nv; base += 32 * U) {
+        uint4 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + 32 * u;
+          if (idx < nv) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q[u].x), "=r"(q[u].y), "=r"(q[u].z), "=r"(q[u].w) : "l"(row + idx));
+          else q[u] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= q[u].x ^ q[u].y ^ q[u].z ^ q[u].w;
+      }
+    }
+  } else {
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+      const uint4* row = A + (size_t)perm[i] * ldv;
+      for (int base = threadIdx.x; base < nv; base += 256 * U) {
+        uint4 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + 256 * u;
+          if (idx < nv) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q[u].x), "=r"(q[u].y), "=r"(q[u].z), "=r"(q[u].w) : "l"(row + idx));
+          else q[u] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= q[u].x ^ q[u].y ^ q[u].z ^ q[u].w;
+      }
+    }
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+static float h2f(__half h) { return __half2float(h); }
+
+int main(int argc, char** argv) {
+  int n = argc > 1 ? atoi(argv[1]) : 16384;
+  int reps = argc > 2 ? atoi(argv[2]) : 20;
+  const int B = 64, nb = (n + B - 1) / B;
+  const size_t ld = (n + 31) & ~31;
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<double> U(-1.0, 1.0);
+  std::vector<float> A((size_t)n * ld, 0.f), v(n);
+  std::vector<__half> LU((size_t)n * ld, __float2half(0.f));
+  std::vector<int> perm(n);
+  for (size_t i = 0; i < (size_t)n; ++i)
+    for (int j = 0; j < n; ++j) A[i * ld + j] = (float)U(rng);
+  for (int j = 0; j < n; ++j) v[j] = (float)U(rng);
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  if (!getenv("OPSEG_IDPERM")) std::shuffle(perm.begin(), perm.end(), rng);
+  const double sc = 0.5 / std::sqrt((double)n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double x = (i == j) ? 1.0 + 0.5 * std::fabs(U(rng)) : sc * U(rng);
+      LU[(size_t)i * ld + j] = __float2half((float)x);
+    }
+  // block inverse records (col-major, hi), strictly lower (unit diag implied) / full upper
+  const size_t RS = 2 * B * B;
+  std::vector<double> linv(nb * RS, 0.0), uinv(nb * RS, 0.0);
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = b * B, m = std::min(B, n - r0);
+    for (int c = 0; c < m; ++c) {
+      std::vector<double> x(B, 0.0);
+      x[c] = 1.0;
+      for (int i = c + 1; i < m; ++i) {
+        double s = 0;
+        for (int j = c; j < i; ++j) s += h2f(LU[(size_t)(r0 + i) * ld + r0 + j]) * x[j];
+        x[i] = -s;
+      }
+      for (int i = c + 1; i < m; ++i) linv[b * RS + c * B + i] = x[i];
+      std::fill(x.begin(), x.end(), 0.0);
+      x[c] = 1.0 / h2f(LU[(size_t)(r0 + c) * ld + r0 + c]);
+      for (int i = c - 1; i >= 0; --i) {
+        double s = 0;
+        for (int j = i + 1; j <= c; ++j) s += h2f(LU[(size_t)(r0 + i) * ld + r0 + j]) * x[j];
+        x[i] = -s / h2f(LU[(size_t)(r0 + i) * ld + r0 + i]);
+      }
+      for (int i = 0; i <= c; ++i) uinv[b * RS + c * B + i] = x[i];
+    }
+  }
+  // folded neighbour blocks: lower M_b = D_b^-1 L_{b,b-1}, upper M_b = U_bb^-1 U_{b,b+1} (row-major)
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = b * B, m = std::min(B, n - r0);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < B; ++j) {
+        if (b >= 1) {
+          const int c = (b - 1) * B + j;
+          double sl = h2f(LU[(size_t)(r0 + i) * ld + c]);
+          for (int k = 0; k < i; ++k) sl += linv[b * RS + k * B + i] * h2f(LU[(size_t)(r0 + k) * ld + c]);
+          linv[b * RS + B * B + i * B + j] = sl;
+        }
+        if (b + 1 < nb) {
+          const int c = (b + 1) * B + j;
+          double su = 0;
+          if (c < n)
+            for (int k = i; k < m; ++k) su += uinv[b * RS + k * B + i] * h2f(LU[(size_t)(r0 + k) * ld + c]);
+          uinv[b * RS + B * B + i * B + j] = su;
+        }
+      }
+  }
+  // host reference
+  std::vector<double> t(n), y(n), z(n);
+  for (int i = 0; i < n; ++i) {
+    double s = 0;
+    const float* row = &A[(size_t)perm[i] * ld];
+    for (int j = 0; j < n; ++j) s += (double)row[j] * v[j];
+    t[i] = s;
+  }
+  for (int i = 0; i < n; ++i) {
+    double s = t[i];
+    for (int j = 0; j < i; ++j) s -= h2f(LU[(size_t)i * ld + j]) * y[j];
+    y[i] = s;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int j = i + 1; j < n; ++j) s -= h2f(LU[(size_t)i * ld + j]) * z[j];
+    z[i] = s / h2f(LU[(size_t)i * ld + i]);
+  }
+  // device
+  float *dA, *dv, *dw;
+  __half* dLU;
+  int* dperm;
+  double *dlinv, *duinv, *dt;
+  uint4 *dtl, *dtu, *dpl, *dpu;
+  GridCtl* dctl;
+  unsigned long long* dst;
+  cudaMalloc(&dA, sizeof(float) * A.size());
+  cudaMalloc(&dv, sizeof(float) * n);
+  cudaMalloc(&dw, sizeof(float) * n);
+  cudaMalloc(&dLU, sizeof(__half) * LU.size());
+  cudaMalloc(&dperm, sizeof(int) * n);
+  cudaMalloc(&dlinv, sizeof(double) * linv.size());
+  cudaMalloc(&duinv, sizeof(double) * uinv.size());
+  cudaMalloc(&dt, sizeof(double) * n);
+  cudaMalloc(&dtl, sizeof(uint4) * n);
+  cudaMalloc(&dtu, sizeof(uint4) * n);
+  cudaMalloc(&dpl, sizeof(uint4) * n);
+  cudaMalloc(&dpu, sizeof(uint4) * n);
+  cudaMemset(dpl, 0, sizeof(uint4) * n);
+  cudaMemset(dpu, 0, sizeof(uint4) * n);
+  cudaMalloc(&dctl, sizeof(GridCtl));
+  cudaMalloc(&dst, 8 * (8 + 16 * 1024));
+  cudaMemcpy(dA, A.data(), sizeof(float) * A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dv, v.data(), sizeof(float) * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dLU, LU.data(), sizeof(__half) * LU.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dperm, perm.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dlinv, linv.data(), sizeof(double) * linv.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(duinv, uinv.data(), sizeof(double) * uinv.size(), cudaMemcpyHostToDevice);
+  cudaMemset(dtl, 0, sizeof(uint4) * n);
+  cudaMemset(dtu, 0, sizeof(uint4) * n);
+  cudaMemset(dctl, 0, sizeof(GridCtl));
+  double *dlbig, *dubig, *ysc;
+  const int nK = (n + NBIG - 1) / NBIG;
+  cudaMalloc(&dlbig, sizeof(double) * (size_t)nK * NBIG * NBIG);
+  cudaMalloc(&dubig, sizeof(double) * (size_t)nK * NBIG * NBIG);
+  cudaMalloc(&ysc, sizeof(double) * n);
+  {
+    cudaEvent_t i0, i1; cudaEventCreate(&i0); cudaEventCreate(&i1);
+    cudaFuncSetAttribute(seg::k_bigblock_inverse<__half, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * NBIG * 8);
+    cudaFuncSetAttribute(seg::k_bigblock_inverse<__half, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * NBIG * 8);
+    cudaEventRecord(i0);
+    seg::k_bigblock_inverse<__half, true><<<148 * 4, 256, 8 * NBIG * 8>>>(dLU, ld, n, NBIG, dlbig);
+    seg::k_bigblock_inverse<__half, false><<<148 * 4, 256, 8 * NBIG * 8>>>(dLU, ld, n, NBIG, dubig);
+    cudaEventRecord(i1); cudaEventSynchronize(i1);
+    float ms; cudaEventElapsedTime(&ms, i0, i1);
+    printf("big-block inverses (NB=%d): %.2f ms (%s)\n", NBIG, ms, cudaGetErrorString(cudaGetLastError()));
+  }
+  int G = 148;
+  const size_t budget = 220 * 1024;
+  int gstages = seg::gemv_stages(n, budget);
+  #if KSEG == -1
+  size_t smem = seg::gemv_smem(n, gstages);
+#elif KSEG == 0
+  size_t smem = std::max(seg::sweep2_smem(2), seg::gemv_smem(n, gstages));
+#else
+  size_t smem = std::max(seg::sweep_smem<KSEG, __half>(), seg::gemv_smem(n, gstages));
+#endif
+  printf("smem %zu B, gemv stages %d\n", smem, gstages);
+  cudaFuncSetAttribute(k_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  unsigned epoch = 0;
+  auto launch = [&](int phases, unsigned long long* stamps) {
+    size_t ldz = ld;
+    void* args[] = {&n, &dA, &ldz, &dperm, &dv, &dLU, &ldz, &dlinv, &duinv, &dt, &dtl, &dtu, &dpl, &dpu, &dw, &dctl, &epoch, &phases, &stamps, &gstages, &dlbig, &dubig, &ysc};
+    cudaMemsetAsync(dctl, 0, sizeof(unsigned), 0);
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)k_op, dim3(G), dim3(256), args, smem, 0);
+    ++epoch;
+    return e;
+  };
+  if (getenv("OPSEG_PROF")) {
+    int ph = atoi(getenv("OPSEG_PROF"));
+    for (int i = 0; i < 4; ++i) launch(ph, nullptr);
+    cudaDeviceSynchronize();
+    printf("prof run phases=%d: %s\n", ph, cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
+  if (launch(7, dst) != cudaSuccess) { printf("launch failed: %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("run failed: %s\n", cudaGetErrorString(e)); return 1; }
+  if (KSEG >= 0) {
+    std::vector<double> tg(n);
+    cudaMemcpy(tg.data(), dt, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    double te = 0, tm = 0;
+    for (int i = 0; i < n; ++i) { te = std::max(te, std::fabs(tg[i] - t[i])); tm = std::max(tm, std::fabs(t[i])); }
+    std::vector<uint4> yl(n);
+    cudaMemcpy(yl.data(), dtl, sizeof(uint4) * n, cudaMemcpyDeviceToHost);
+    double ye = 0, ym = 0;
+    for (int i = 0; i < n; ++i) {
+      unsigned long long b = ((unsigned long long)yl[i].z << 32) | yl[i].x;
+      double yv; memcpy(&yv, &b, 8);
+      ye = std::max(ye, std::fabs(yv - y[i])); ym = std::max(ym, std::fabs(y[i]));
+    }
+    printf("check t: max abs err %.3e (|t| %.3e); forward y: %.3e (|y| %.3e)\n", te, tm, ye, ym);
+  }
+  std::vector<float> w(n);
+  cudaMemcpy(w.data(), dw, sizeof(float) * n, cudaMemcpyDeviceToHost);
+  double maxerr = 0, zmax = 0; int nbad = 0;
+  for (int i = 0; i < n; ++i) {
+    double ref = (double)(float)z[i];
+    double err = std::fabs((double)w[i] - ref);
+    if (err > 2.0 * std::ldexp(std::fabs(ref), -23) + 1e-30) ++nbad;
+    maxerr = std::max(maxerr, err / std::max(std::fabs(ref), 1e-300));
+    zmax = std::max(zmax, std::fabs(z[i]));
+  }
+  printf("n=%d K=%d check: max rel err %.3e, entries beyond 2 ulp(fp32): %d, |z|max %.3e\n", n, KSEG, maxerr, nbad, zmax);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const double bytes = (double)n * n * (4 + 2);
+  for (int ph : {7, 1, 8, 128, 6}) {
+    for (int i = 0; i < 3; ++i) launch(ph, nullptr);
+    cudaEventRecord(e0);
+    for (int i = 0; i < reps; ++i) launch(ph, nullptr);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    printf("phases=%d: %.1f us per launch", ph, ms * 1e3);
+    if (ph == 7) printf("  (%.0f GB/s algorithmic = n^2 (4 + 2) B)", bytes / (ms * 1e-3) / 1e9);
+    printf("\n");
+  }
+  for (int grid : {148 * 8, 148 * 32}) {
+    for (int i = 0; i < 3; ++i) k_stream<<<grid, 256>>>((const uint4*)dA, A.size() / 4, dt);
+    cudaEventRecord(e0);
+    for (int i = 0; i < reps; ++i) k_stream<<<grid, 256>>>((const uint4*)dA, A.size() / 4, dt);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    printf("stream read of A (%zu MB), grid %d: %.1f us = %.0f GB/s\n", A.size() * 4 >> 20, grid, ms * 1e3, A.size() * 4.0 / (ms * 1e-3) / 1e9);
+  }
+  {
+    auto probe = [&](const char* name, auto kern) {
+      const int nv = (int)(ld / 4);
+      for (int i = 0; i < 3; ++i) kern<<<148, 256>>>((const uint4*)dA, ld / 4, dperm, n, nv, dt);
+      cudaEventRecord(e0);
+      for (int i = 0; i < reps; ++i) kern<<<148, 256>>>((const uint4*)dA, ld / 4, dperm, n, nv, dt);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= reps;
+      printf("%s: %.1f us = %.0f GB/s\n", name, ms * 1e3, A.size() * 4.0 / (ms * 1e-3) / 1e9);
+    };
+    probe("rowstream warp/row U=8", k_rowstream<8, false>);
+    probe("rowstream warp/row U=16", k_rowstream<16, false>);
+    probe("rowstream cta/row U=4", k_rowstream<4, false + 1>);
+    probe("rowstream cta/row U=8", k_rowstream<8, true>);
+  }
+  launch(7, dst);
+  cudaDeviceSynchronize();
+  unsigned long long hs[2];
+  cudaMemcpy(hs, dst, 16, cudaMemcpyDeviceToHost);
+  printf("in-kernel: gemv %.1f us, sweeps %.1f us\n", hs[0] / 1e3, hs[1] / 1e3);
+  if (KSEG >= 0) {
+    const int nseg = KSEG > 0 ? (nb + KSEG - 1) / KSEG : nb;
+    std::vector<unsigned long long> st(16 * 1024);
+    cudaMemcpy(st.data(), dst + 8, 8 * 16 * 1024, cudaMemcpyDeviceToHost);
+    for (int sw = 0; sw < 2; ++sw) {
+      const unsigned long long* S = st.data() + sw * 8 * 1024;
+      unsigned long long t0 = S[0];
+      for (int i = 0; i < nseg; ++i) t0 = std::min(t0, S[8 * i]);
+      double a = 0, b = 0, c = 0, d = 0; int cnt = 0;
+      for (int i = 1; i < nseg; ++i) {
+        double pub = (double)S[8 * (i - 1) + 3];
+        a += (double)S[8 * i + 4] - pub;        // prev publish -> last block seen
+        b += (double)S[8 * i + 5] - (double)S[8 * i + 4];  // seen -> after stage sync
+        c += (double)S[8 * i + 2] - (double)S[8 * i + 5];  // -> solve start (compute + reduce)
+        d += (double)S[8 * i + 3] - (double)S[8 * i + 2];  // local solve
+        ++cnt;
+      }
+      if (KSEG == 0) {
+        double h = 0, f = 0, ffl = 0, prl = 0, seenl = 0; int late = 0, cnt = 0;
+        for (int i = 1; i < nseg; ++i) {
+          h += (double)S[8 * i + 4] - (double)S[8 * (i - 1) + 3];
+          f += (double)S[8 * i + 3] - (double)S[8 * i + 4];
+          late += S[8 * i + 1] > S[8 * (i - 1) + 3];
+        }
+        for (int i = 3; i < nseg; ++i) {
+          ffl += (double)S[8 * i + 5] - (double)S[8 * (i - 3) + 3];   // far field done after pub(b-3)
+          prl += (double)S[8 * i + 1] - (double)S[8 * (i - 2) + 3];   // pre done after pub(b-2)
+          seenl += (double)S[8 * i + 4] - (double)S[8 * (i - 1) + 3]; // y_{b-1} seen after its pub
+          ++cnt;
+        }
+        printf("sweep %s: end %.1f us; per block (ns): publish->seen %.0f, seen->publish %.0f; pre late on %d of %d\n",
+               sw ? "U" : "L", (S[8 * (nseg - 1) + 3] - t0) / 1e3, h / (nseg - 1), f / (nseg - 1), late, nseg - 1);
+        printf("   far done - pub(b-3) %.0f ns, pre done - pub(b-2) %.0f ns, seen(b-1) - pub(b-1) %.0f ns\n", ffl / cnt, prl / cnt, seenl / cnt);
+      } else
+      printf("sweep %s: end %.1f us; per segment (ns): publish->seen %.0f, seen->synced %.0f, ->solve start %.0f, solve %.0f\n",
+             sw ? "U" : "L", (S[8 * (nseg - 1) + 3] - t0) / 1e3, a / cnt, b / cnt, c / cnt, d / cnt);
+    }
+  }
+  e = cudaGetLastError();
+  printf("status: %s\n", cudaGetErrorString(e));
+  return 0;
+}
