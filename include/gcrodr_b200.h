@@ -138,6 +138,13 @@ gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out);
  * parity checks run the step with max_cycles = 1.  No reference counterpart. */
 gb_status gb_debug_hessenberg(gb_solver* s, double* h);
 
+/* diagnostics: lower the cycle cap of subsequent steps to `cycles`
+ * (1 <= cycles <= the max_cycles the solver was created with).  Mirrors
+ * calling gmres_solve / gcrodr_solve with a smaller GmresConfig.max_cycles
+ * (gmres.py:51-54, gcrodr.py:86-89): per-cycle parity checks run one cycle
+ * at a time, the bench truncates its warm-up solves with it. */
+gb_status gb_debug_set_max_cycles(gb_solver* s, int cycles);
+
 /* number of kernels this library has launched (process-wide) */
 long long gb_launch_count(void);
 

@@ -29,7 +29,7 @@ EXPORTS = [
     "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
     "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog", "gb_time_op",
-    "gb_debug_hessenberg",
+    "gb_debug_hessenberg", "gb_debug_set_max_cycles",
 ]
 
 
@@ -104,6 +104,7 @@ def load(path: str | None = None):
         "gb_debug_phaselog": (C.c_int, [vp, C.c_int, vp]),
         "gb_time_op": (C.c_int, [vp, C.c_int, C.c_int, dp]),
         "gb_debug_hessenberg": (C.c_int, [vp, vp]),
+        "gb_debug_set_max_cycles": (C.c_int, [vp, C.c_int]),
         "gb_last_factor_ms": (C.c_double, [vp]),
         "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
                                        vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
@@ -216,6 +217,10 @@ class Solver:
         info = StepInfo()
         _check(self.lib.gb_refine_step(self.h, C.byref(info)), "gb_refine_step")
         return info
+
+    def set_max_cycles(self, cycles: int) -> None:
+        """Lower the cycle cap of subsequent steps (<= the cap at creation)."""
+        _check(self.lib.gb_debug_set_max_cycles(self.h, int(cycles)), "gb_debug_set_max_cycles")
 
     def last_cycles(self) -> tuple[list[int], list[int]]:
         cap = self.opts.max_cycles + 1

@@ -5,6 +5,8 @@
 #include <cstring>
 #include "gb_solver.cuh"
 
+thread_local std::string g_err;
+
 const VariantOps* gb_variant_f_h_f64() __attribute__((weak));
 const VariantOps* gb_variant_f_h_f32() __attribute__((weak));
 const VariantOps* gb_variant_f_f_f64() __attribute__((weak));
@@ -72,6 +74,7 @@ gb_status gb_solver_create(gb_solver** out, int n, const gb_options* opt, void* 
   gb_solver* s = new gb_solver();
   s->n = n;
   s->o = o;
+  s->max_cycles_cap = o.max_cycles;
   s->stream = (cudaStream_t)stream;
   s->ldv = (n + 31) & ~31;
   s->lda = (n + 31) & ~31;
@@ -161,7 +164,7 @@ gb_status gb_refine_step(gb_solver* s, gb_step_info* info) {
 
 gb_status gb_last_cycles(gb_solver* s, int* iters, int* keff, int cap, int* ncycles) {
   if (!s) return fail(GB_ERR_ARG, "null solver");
-  int c = std::min(cap, s->o.max_cycles + 1);
+  int c = std::min(cap, s->max_cycles_cap + 1);
   CK(cudaMemcpyAsync(iters, s->cycle_iters, sizeof(int) * c, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaMemcpyAsync(keff, s->cycle_keff, sizeof(int) * c, cudaMemcpyDeviceToHost, s->stream));
   gb_step_info inf;
@@ -232,6 +235,14 @@ gb_status gb_debug_hessenberg(gb_solver* s, double* h) {
   if (!s || !h) return fail(GB_ERR_ARG, "null argument");
   CK(cudaMemcpyAsync(h, s->H, sizeof(double) * (size_t)(s->o.m + 1) * s->o.m, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
+  return GB_OK;
+}
+
+gb_status gb_debug_set_max_cycles(gb_solver* s, int cycles) {
+  if (!s) return fail(GB_ERR_ARG, "null solver");
+  if (cycles < 1 || cycles > s->max_cycles_cap)
+    return fail(GB_ERR_ARG, "cycles must lie in [1, max_cycles at creation]");
+  s->o.max_cycles = cycles;
   return GB_OK;
 }
 

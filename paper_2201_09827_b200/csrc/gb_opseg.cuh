@@ -831,6 +831,145 @@ __device__ __noinline__ void sweep_bsp(Team& t, int n, int NB, const TF* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Look-ahead form of sweep_bsp (same arithmetic, same per-row summation order,
+// so bit-identical results): after y_K is known only the rows of the NEXT
+// block are updated before the barrier (phase A, NB rows); the solve of that
+// block, y_{K+1} = D_{K+1}^-1 s_{K+1}, then runs in the same phase as the
+// update of all the later rows with y_K (phase B), which hides the
+// latency-bound triangular product behind the streamed panel.
+// smem: 2 NB doubles (y_K | s_{K+1}).
+// ---------------------------------------------------------------------------
+template <bool kLower>
+GB_DEVICE double bsp_diag_row(const double* __restrict__ D, int NB, int r, int m, const double* vs, int lane) {
+  const double2* drow = reinterpret_cast<const double2*>(D + (size_t)r * NB);
+  const int v0 = kLower ? 0 : (r >> 1), v1 = kLower ? (r >> 1) + 1 : (m + 1) >> 1;  // double2 range
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int base = v0 + lane; base < v1; base += 32 * 16) {
+    double2 d2[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int v = base + 32 * u;
+      d2[u] = v < v1 ? __ldg(drow + v) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int v = base + 32 * u;
+      if (v < v1) {
+        a[u & 1] = __fma_rn(d2[u].x, vs[2 * v], a[u & 1]);
+        a[2 + (u & 1)] = __fma_rn(d2[u].y, vs[2 * v + 1], a[2 + (u & 1)]);
+      }
+    }
+  }
+  double s = __dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return s;
+}
+
+// s[r] -= F[r][c0 .. c0+m) . y  for rows r and (two ? r2 : none); vs = y in smem
+template <class TF>
+GB_DEVICE void bsp_update_rows(const TF* __restrict__ LU, size_t ldf, int c0, int m, int r, int r2, bool two,
+                               const double* vs, double* ybuf, int lane) {
+  constexpr int VW = 16 / sizeof(TF);
+  const int nv = (m + VW - 1) / VW;
+  const uint4* f0 = reinterpret_cast<const uint4*>(LU + (size_t)r * ldf + c0);
+  const uint4* f1 = reinterpret_cast<const uint4*>(LU + (size_t)(two ? r2 : r) * ldf + c0);
+  double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int base = lane; base < nv; base += 32 * 8) {
+    uint4 q0[8], q1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int v = base + 32 * u;
+      q0[u] = v < nv ? __ldg(f0 + v) : make_uint4(0, 0, 0, 0);
+      q1[u] = (v < nv && two) ? __ldg(f1 + v) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int v = base + 32 * u;
+      if (v < nv) {
+        const TF* e0 = reinterpret_cast<const TF*>(&q0[u]);
+        const TF* e1 = reinterpret_cast<const TF*>(&q1[u]);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) {
+          const double y = vs[v * VW + j];
+          a[j & 3] = __fma_rn(f2d<TF>(e0[j]), y, a[j & 3]);
+          b[j & 3] = __fma_rn(f2d<TF>(e1[j]), y, b[j & 3]);
+        }
+      }
+    }
+  }
+  double s0 = __dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3]));
+  double s1 = __dadd_rn(__dadd_rn(b[0], b[1]), __dadd_rn(b[2], b[3]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 = __dadd_rn(s0, __shfl_xor_sync(0xffffffffu, s0, o));
+    s1 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+  }
+  if (lane == 0) {
+    ybuf[r] = __dsub_rn(ybuf[r], s0);
+    if (two) ybuf[r2] = __dsub_rn(ybuf[r2], s1);
+  }
+}
+
+template <class TF, bool kLower, class Team, class Out>
+__device__ __noinline__ void sweep_la(Team& t, int n, int NB, const TF* __restrict__ LU, size_t ldf,
+                                     const double* __restrict__ dinv, double* ybuf, double* ysol, Out out,
+                                     void* smem_raw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int W = t.size() * (NT / 32);
+  const int gw = t.rank() * (NT / 32) + wid;
+  const int nK = (n + NB - 1) / NB;
+  double* vy = reinterpret_cast<double*>(smem_raw);  // [NB]: y_K
+  double* vs = vy + NB;                              // [NB]: s_{K+1}
+  auto blk = [&](int it) { return kLower ? it : nK - 1 - it; };
+  auto solve_block = [&](int K) {
+    const int r0 = K * NB, m = min(NB, n - r0);
+    const double* D = dinv + (size_t)K * NB * NB;
+    for (int r = gw; r < m; r += W) {
+      const double s = bsp_diag_row<kLower>(D, NB, r, m, vs, lane);
+      if (lane == 0) {
+        ysol[r0 + r] = s;
+        out(r0 + r, s);
+      }
+    }
+  };
+  // prologue: first block of the sweep
+  {
+    const int K = blk(0), r0 = K * NB, m = min(NB, n - r0);
+    for (int c = threadIdx.x; c < NB; c += NT) vs[c] = c < m ? __ldcg(ybuf + r0 + c) : 0.0;
+    __syncthreads();
+    solve_block(K);
+    t.sync();
+  }
+  for (int it = 0; it + 1 < nK; ++it) {
+    const int K = blk(it), K1 = blk(it + 1);
+    const int r0 = K * NB, m = min(NB, n - r0);
+    const int q0 = K1 * NB, mq = min(NB, n - q0);
+    for (int c = threadIdx.x; c < NB; c += NT) vy[c] = c < m ? __ldcg(ysol + r0 + c) : 0.0;
+    __syncthreads();
+    // phase A: the next block's rows
+    for (int r = gw; r < mq; r += 2 * W) {
+      const bool two = r + W < mq;
+      bsp_update_rows<TF>(LU, ldf, r0, m, q0 + r, q0 + r + W, two, vy, ybuf, lane);
+    }
+    t.sync();
+    // phase B: solve the next block | update every later row with y_K
+    for (int c = threadIdx.x; c < NB; c += NT) vs[c] = c < mq ? __ldcg(ybuf + q0 + c) : 0.0;
+    __syncthreads();
+    solve_block(K1);
+    const int lo = kLower ? q0 + mq : 0, hi = kLower ? n : q0;
+    // rotate the warp numbering past the warps that took a second solve row
+    const int rot = mq % W;
+    const int gw2 = (gw + W - rot) % W;
+    for (int r = lo + gw2; r < hi; r += 2 * W) {
+      const bool two = r + W < hi;
+      bsp_update_rows<TF>(LU, ldf, r0, m, r, r + W, two, vy, ybuf, lane);
+    }
+    t.sync();
+  }
+}
+
 // D_K^-1 for the NB x NB diagonal blocks of the unit lower (kLower) or upper
 // factor, row-major fp64, one warp per column: forward (backward)
 // substitution of e_c with warp-parallel dot products, the column kept in

@@ -17,7 +17,9 @@
 
 using namespace gb;
 
-static thread_local std::string g_err;
+// one definition (gb_capi.cu) shared by every precision-variant translation unit,
+// so gb_last_error() reports failures raised inside the variants
+extern thread_local std::string g_err;
 // kernels launched by this library (gb_launch_count); counted at launch sites
 extern long long* gb_launch_counter();
 static inline void count_launch(long long k = 1) { __atomic_fetch_add(gb_launch_counter(), k, __ATOMIC_RELAXED); }
@@ -786,6 +788,7 @@ struct gb_solver {
   // (gb_opseg.cuh sweep_bsp), GEMV bulk-copy stages, A entries all normal
   double *bigl = nullptr, *bigu = nullptr;
   int nbig = 0, gemv_ns = 0, a_normal = 0;
+  int max_cycles_cap = 0;  // o.max_cycles at creation (workspace size); o.max_cycles may be lowered
   PivKey* lu_ckey = nullptr;
   double *lu_crow = nullptr, *lu_rowk = nullptr;
   int* lu_piv = nullptr;
@@ -1132,7 +1135,9 @@ struct Impl {
     a.base = (char*)s->mem;
     plan(true);
     if (s->bigl != nullptr) {
-      const size_t budget = 227 * 1024 - sm_doubles(s->o.m, s->o.k) * sizeof(double) - 1024;
+      // 227 KB per CTA = dynamic + static: the step kernels declare 7 KB of
+      // static shared memory (reduction / pivot scratch), reserve 8 KB for it
+      const size_t budget = 227 * 1024 - sm_doubles(s->o.m, s->o.k) * sizeof(double) - 8192;
       s->gemv_ns = (budget > seg::gemv_vbytes(n) + 4608 + 2 * seg::GCH) ? seg::gemv_stages(n, budget) : 0;
     }
     CK(cudaMemsetAsync(s->mem, 0, bytes, s->stream));

@@ -21,6 +21,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <algorithm>
 
 #include "gb_tc.cuh"
 
@@ -242,4 +243,241 @@ inline cudaError_t tc_update(__half* W, size_t ld, int nrows, int r0, int c0, in
 }
 
 }  // namespace tcg
+
+// ---------------------------------------------------------------------------
+// CTA-pair form of the same update (cta_group::2): a cluster of two CTAs on
+// one TPC owns a 256 x 256 tile of C.  Each CTA stages its own 128 rows of A
+// and its own 128 of the 256 Bt rows (16 KB per 32-wide K slab instead of the
+// 24 KB of the one-CTA kernel, which the L2 -> SM path caps at ~44 % of the
+// tensor peak: ~42 B/clk/SM against the 96 B/clk/SM a 128 x 256 tile needs);
+// the leader's elected thread issues tcgen05.mma.cta_group::2 (M = 256,
+// N = 256), which reads the B halves out of both CTAs' shared memory and
+// leaves rows 128 r .. 128 r + 127 of the accumulator in CTA r's TMEM.
+//   full[s]    lives in the leader: its producer arms 2 x 16 KB, both CTAs'
+//              TMA loads complete_tx on it (cta_group::2 form);
+//   empty[s], tfull[a]  are signalled in both CTAs by the multicast commit;
+//   tempty[a]  lives in the leader: the 8 epilogue warps of the pair arrive.
+// ---------------------------------------------------------------------------
+namespace tcg2 {
+
+constexpr int BM = 128, PM = 256, BN = 256, HN = 128, BK = 32;
+constexpr int STAGES = 12;
+constexpr int A_BYTES = BM * BK * 2;            // 8 KB
+constexpr int B_BYTES = HN * BK * 2;            // 8 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 16 KB per CTA
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
+constexpr int NTHREADS = 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of the leader CTA's copy of a shared-memory object, in the cluster window
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(tc::smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// completion of all prior MMAs of the pair -> the barrier at this offset in both CTAs
+__device__ __forceinline__ void commit_pair(uint64_t* mbar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          tc::smem_u32(mbar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_tc_update2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, __half* W,
+                 size_t ld, int r0, int c0, int M, int N, int k0, int K) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // the same offset in both CTAs (the dynamic window starts at the same address)
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tm = (M + PM - 1) / PM, tn = (N + BN - 1) / BN;
+  const int ntiles = tm * tn;
+  const int nslab = K / BK;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      tc::mbar_init(full + i, 1);
+      tc::mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(tfull + i, 1);
+      tc::mbar_init(tempty + i, 8);  // one elected arrive per epilogue warp of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tcg::prefetch_map(&map_a);
+    tcg::prefetch_map(&map_b);
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc::fence_before();
+  cluster_sync_all();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer (both CTAs): own 128 rows of A, own 128 rows of Bt
+    int st = 0;
+    uint32_t ph = 0;
+    for (int t = pair; t < ntiles; t += npairs) {
+      const int ti = t / tn, tj = t % tn;
+      for (int s = 0; s < nslab; ++s) {
+        tc::mbar_wait(empty + st, ph ^ 1u);
+        unsigned char* sa = smem + st * STAGE_BYTES;
+        unsigned char* sb = sa + A_BYTES;
+        if (rank == 0) tcg::mbar_expect_tx(full + st, 2 * STAGE_BYTES);
+        const uint32_t bar = leader_addr(full + st);
+        tma_2d_pair(sa, &map_a, k0 + s * BK, r0 + ti * PM + (int)rank * BM, bar);
+        tma_2d_pair(sb, &map_b, s * BK, tj * BN + (int)rank * HN, bar);
+        if (++st == STAGES) st = 0, ph ^= 1u;
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---- MMA issuer: one thread of the leader CTA for the pair
+    constexpr uint32_t idesc = tc::idesc_f16_f32(PM, BN);
+    int st = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      const int acc = it & 1;
+      const uint32_t aph = (uint32_t)((it >> 1) & 1);
+      tc::mbar_wait(tempty + acc, aph ^ 1u);  // both CTAs' epilogues drained this accumulator
+      tc::fence_after();
+      const uint32_t dt = tmem + (uint32_t)(acc * BN);
+      for (int s = 0; s < nslab; ++s) {
+        tc::mbar_wait(full + st, ph);
+        tc::fence_after();
+        const unsigned char* sa = smem + st * STAGE_BYTES;
+        const uint64_t ad = tc::desc_k64(tc::smem_u32(sa)), bd = tc::desc_k64(tc::smem_u32(sa + A_BYTES));
+        mma_f16_pair(dt, ad, bd, idesc, s > 0 ? 1u : 0u);
+        mma_f16_pair(dt, ad + 2, bd + 2, idesc, 1u);
+        commit_pair(empty + st);
+        if (++st == STAGES) st = 0, ph ^= 1u;
+      }
+      commit_pair(tfull + acc);
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue (both CTAs): row = TMEM lane = row 128 rank + lane of the pair tile
+    const int q = warp - 4;
+    const int row_in_tile = (int)rank * BM + q * 32 + lane;
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      const int ti = t / tn, tj = t % tn;
+      const int acc = it & 1;
+      tc::mbar_wait(tfull + acc, (uint32_t)((it >> 1) & 1));
+      tc::fence_after();
+      const int gi = ti * PM + row_in_tile;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tc::tmem_ld32(tbase + (uint32_t)(ch * 32), v);
+        const int gj = tj * BN + ch * 32;
+        if (gi < M && gj < N) {
+          __half* p = W + (size_t)(r0 + gi) * ld + c0 + gj;
+          if (gj + 32 <= N) {
+            __align__(16) __half h[32];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) reinterpret_cast<uint4*>(h)[z] = reinterpret_cast<const uint4*>(p)[z];
+#pragma unroll
+            for (int z = 0; z < 32; ++z) h[z] = __float2half_rn(__half2float(h[z]) - v[z]);
+#pragma unroll
+            for (int z = 0; z < 4; ++z) reinterpret_cast<uint4*>(p)[z] = reinterpret_cast<const uint4*>(h)[z];
+          } else {
+            for (int z = 0; z < 32 && gj + z < N; ++z) p[z] = __float2half_rn(__half2float(p[z]) - v[z]);
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_addr(tempty + acc));
+    }
+  }
+  tc::fence_before();
+  cluster_sync_all();  // the leader's MMAs read the peer's shared memory; remote arrives target the leader
+  if (warp == 2) tmem_dealloc_pair(tmem, 512);
+}
+
+// pairs that can be co-resident (148 SMs = 74 TPCs unless a GPC is short)
+inline int max_pairs() {
+  static int pairs = -1;
+  if (pairs < 0) {
+    cudaFuncSetAttribute(k_tc_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 74);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)k_tc_update2, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 64;
+    }
+    pairs = n;
+  }
+  return pairs;
+}
+
+// same contract as tcg::tc_update
+inline cudaError_t tc_update(__half* W, size_t ld, int nrows, int r0, int c0, int M, int N, int k0, int K,
+                             __half* Bt, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  dim3 tb(32, 8), tg((N + 31) / 32, (K + 31) / 32);
+  tcg::k_transpose_u12<<<tg, tb, 0, st>>>(W, ld, k0, c0, K, N, Bt);
+  CUtensorMap ma, mb;
+  if (!tcg::make_map(&ma, W, (uint64_t)nrows, ld, ld, BM) || !tcg::make_map(&mb, Bt, (uint64_t)N, (uint64_t)K, K, HN))
+    return cudaErrorInvalidValue;
+  const int ntiles = ((M + PM - 1) / PM) * ((N + BN - 1) / BN);
+  const int pairs = std::min(ntiles, max_pairs());
+  k_tc_update2<<<2 * pairs, NTHREADS, SMEM_BYTES, st>>>(ma, mb, W, ld, r0, c0, M, N, k0, K);
+  return cudaGetLastError();
+}
+
+}  // namespace tcg2
 }  // namespace gb

@@ -45,7 +45,27 @@ VARIANTS = {
     **{f"ulp{s}": (False, False, f"ulp{s}") for s in range(8)},
     # unblocked fp32 LU together with a last-bit move of the first update
     **{f"lu_ulp{s}": (False, True, f"ulp{s}") for s in range(4)},
+    # the operator's result moved by a random {-1, 0, +1} ulp of u per entry
+    # (seed S): config 2 runs the operator in double-double through factors
+    # with kappa(U) ~ 1e17, so two dd implementations that differ at the 1e-32
+    # level (summation order, FMA two_prod) differ by ulps of u after rounding
+    **{f"opulp{s}": (False, False, f"opulp{s}") for s in range(8)},
 }
+
+
+def _perturb_operator(seed: int) -> None:
+    rng = np.random.default_rng(1000 + seed)
+    base_op, base_rhs = O.apply_op, O.precond_rhs
+
+    def nudge(w):
+        w = np.asarray(w, dtype=np.float64)
+        step = rng.integers(-1, 2, size=w.shape)
+        up = np.nextafter(w, np.inf)
+        dn = np.nextafter(w, -np.inf)
+        return np.where(step > 0, up, np.where(step < 0, dn, w))
+
+    O.apply_op = lambda a, f, v, fmt, store: nudge(base_op(a, f, v, fmt, store))
+    O.precond_rhs = lambda f, r, fmt, store: nudge(base_rhs(f, r, fmt, store))
 
 
 def run(cfg: str, variant: str) -> dict:
@@ -56,6 +76,10 @@ def run(cfg: str, variant: str) -> dict:
         raise SystemExit("fp16 LU is exact on the GPU: no LU variant for half factors")
     S._MODE["order"] = order if order in ("lanes", "reversed", "wide") else "lanes"
     S._set(lanes, lu, op=False, ulp_seed=int(order[3:]) if order.startswith("ulp") else None)
+    if order.startswith("opulp"):
+        if spec.precisions[1] != "double":
+            raise SystemExit("opulp variants perturb at u = double")
+        _perturb_operator(int(order[5:]))
     t0 = time.perf_counter()
     rep = O.solve(a, b, spec.precisions, "rgmres-ir", spec.m, spec.k, spec.tau, spec.i_max)
     call = rep.inner_calls[0] if rep.inner_calls else None

@@ -337,6 +337,9 @@ CASES = {
     "cfg4": lambda: _big("cfg4", methods=("rgmres-ir", "gmres-ir")),
     "cfg5_1024": lambda: _big("cfg5_1024", 1024, methods=("rgmres-ir", "gmres-ir"),
                               with_solution=True),
+    # the config-5 analogue on the grid-team kernel type (n > 1024): GCRO-DR-IR only
+    # (661 s of reference time + the simulated fp16 LU)
+    "cfg5_2048": lambda: _big("cfg5_2048", 2048, methods=("rgmres-ir",)),
 }
 
 

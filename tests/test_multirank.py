@@ -1,6 +1,6 @@
 """World-size-2 `gloo` run of the multi-GPU decomposition on CPU:
-bench.py shards the batched workload (cfg3) into disjoint per-rank system
-ranges with no data-path collective, single-system workloads run as replicas,
+bench.py splits the batched workload's own systems (cfg3) into disjoint
+contiguous per-rank ranges with no data-path collective, single-system workloads run as replicas,
 and the whole-job time is the max over ranks (the only collective)."""
 
 import dataclasses
@@ -32,7 +32,7 @@ def _worker(rank: int, world: int, port: int, out):
         import bench
         from paper_2201_09827_b200 import problems
 
-        spec = dataclasses.replace(problems.CONFIGS["cfg3"], batch=3)
+        spec = dataclasses.replace(problems.CONFIGS["cfg3"], batch=5)
         idx = list(bench.shard_systems(spec, rank, world))
         a, b = bench._inputs(spec, rank, world)
         digest = hashlib.sha256(a.tobytes() + b.tobytes()).hexdigest()
@@ -59,8 +59,9 @@ def test_two_rank_sharding_and_timing():
         p.join(timeout=60)
         assert p.exitcode == 0
     (i0, d0, ok0, s0, t0), (i1, d1, ok1, s1, t1) = res
-    # cfg3: disjoint, contiguous shards; each rank built its own systems
-    assert i0 == [0, 1, 2] and i1 == [3, 4, 5]
+    # cfg3: the configuration's systems split into disjoint, contiguous shards
+    # (ceil(batch / world) each); each rank built its own systems
+    assert i0 == [0, 1, 2] and i1 == [3, 4]
     assert ok0 and ok1 and d0 != d1
     # single-system workload: replicas of the same system
     assert s0 == s1 == [0]

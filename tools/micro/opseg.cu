@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(256, 1) k_op(int n, const float* A, size_t lda
   unsigned long long t1 = 0;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0) t1 = gtimer();
   seg::SweepIO lo{n, LU, ldf, linv, t, nullptr, 0u, tl, 2 * epoch + 1, stamps ? stamps + 8 : nullptr};
-#if KSEG == -1
+#if KSEG == -2
+  if (phases & 2) seg::sweep_la<__half, true>(team, n, NBIG, LU, ldf, dlbig, t, ysc, OutNone{}, smem);
+#elif KSEG == -1
   if (phases & 2) seg::sweep_bsp<__half, true>(team, n, NBIG, LU, ldf, dlbig, t, ysc, OutNone{}, smem);
 #elif KSEG == 0
   if (phases & 2) seg::sweep2<__half, true>(team, seg::SweepIO2{lo, pl}, smem, OutNone{});
@@ -77,7 +79,9 @@ __global__ void __launch_bounds__(256, 1) k_op(int n, const float* A, size_t lda
   if (phases & 2) seg::sweep<__half, true, KSEG>(team, lo, smem, OutNone{});
 #endif
   seg::SweepIO up{n, LU, ldf, uinv, nullptr, tl, 2 * epoch + 1, tu, 2 * epoch + 2, stamps ? stamps + 8 + 8 * 1024 : nullptr};
-#if KSEG == -1
+#if KSEG == -2
+  if (phases & 4) seg::sweep_la<__half, false>(team, n, NBIG, LU, ldf, dubig, ysc, t, Out32{w}, smem);
+#elif KSEG == -1
   if (phases & 4) seg::sweep_bsp<__half, false>(team, n, NBIG, LU, ldf, dubig, ysc, t, Out32{w}, smem);
 #elif KSEG == 0
   if (phases & 4) seg::sweep2<__half, false>(team, seg::SweepIO2{up, pu}, smem, Out32{w});
@@ -277,8 +281,8 @@ int main(int argc, char** argv) {
   int G = 148;
   const size_t budget = 220 * 1024;
   int gstages = seg::gemv_stages(n, budget);
-  #if KSEG == -1
-  size_t smem = seg::gemv_smem(n, gstages);
+  #if KSEG < 0
+  size_t smem = std::max(seg::gemv_smem(n, gstages), (size_t)NBIG * 16 + 64);
 #elif KSEG == 0
   size_t smem = std::max(seg::sweep2_smem(2), seg::gemv_smem(n, gstages));
 #else
@@ -335,7 +339,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const double bytes = (double)n * n * (4 + 2);
-  for (int ph : {7, 1, 8, 128, 6}) {
+  for (int ph : {7, 1, 128, 6, 2, 4}) {
     for (int i = 0; i < 3; ++i) launch(ph, nullptr);
     cudaEventRecord(e0);
     for (int i = 0; i < reps; ++i) launch(ph, nullptr);

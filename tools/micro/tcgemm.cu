@@ -10,6 +10,7 @@ using namespace gb;
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 8192;
   const int K = argc > 2 ? atoi(argv[2]) : 256;
+  const int pairmode = argc > 3 ? atoi(argv[3]) : 1;  // 1: CTA-pair kernel (cta_group::2), 0: one-CTA kernel
   const size_t ld = (n + 31) & ~31;
   std::mt19937 rng(3);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
@@ -21,7 +22,12 @@ int main(int argc, char** argv) {
   cudaMemcpy(dW, W.data(), W.size() * 2, cudaMemcpyHostToDevice);
   const int k0 = 0, r0 = K, c0 = K, M = n - K, N = n - K;
   int nsm = 148;
-  cudaError_t e = tcg::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, nsm, 0);
+  auto upd = [&]() {
+    return pairmode ? tcg2::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, 0)
+                    : tcg::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, nsm, 0);
+  };
+  if (pairmode) printf("co-resident CTA pairs: %d\n", tcg2::max_pairs());
+  cudaError_t e = upd();
   cudaError_t e2 = cudaDeviceSynchronize();
   printf("n=%d K=%d launch: %s / %s\n", n, K, cudaGetErrorString(e), cudaGetErrorString(e2));
   std::vector<__half> R(W.size());
@@ -45,14 +51,14 @@ int main(int argc, char** argv) {
   // timing: repeated updates (values drift; only the time matters)
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int i = 0; i < 2; ++i) tcg::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, nsm, 0);
+  for (int i = 0; i < 2; ++i) upd();
   const int reps = 10;
   cudaEventRecord(a);
-  for (int i = 0; i < reps; ++i) tcg::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, nsm, 0);
+  for (int i = 0; i < reps; ++i) upd();
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b); ms /= reps;
   const double fl = 2.0 * M * N * K;
-  printf("update M=N=%d K=%d: %.1f us  %.1f TFLOP/s (%.1f%% of 1593.7)  [%s]\n", M, K, ms * 1e3, fl / (ms * 1e-3) / 1e12,
+  printf("update[%s] M=N=%d K=%d: %.1f us  %.1f TFLOP/s (%.1f%% of 1593.7)  [%s]\n", pairmode ? "pair" : "1cta", M, K, ms * 1e3, fl / (ms * 1e-3) / 1e12,
          100 * fl / (ms * 1e-3) / 1e12 / 1593.7, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

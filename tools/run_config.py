@@ -13,13 +13,16 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--method", default="rgmres-ir")
 ap.add_argument("--grid", type=int, default=0)
 ap.add_argument("--imax", type=int, default=None)
+ap.add_argument("--max-cycles", type=int, default=None)
+ap.add_argument("--lu-mode", default="exact")
 args = ap.parse_args()
 spec = problems.CONFIGS[args.cfg]
 t0 = time.perf_counter()
 a, b = problems.config_problem(spec, 0, args.n)
 t1 = time.perf_counter()
 cfg = RefineConfig(PrecisionTriple.parse(*spec.precisions), Method.parse(args.method), m=spec.m,
-                   k=spec.k if args.method.startswith("r") else 0, tau=spec.tau, i_max=args.imax or spec.i_max)
+                   k=spec.k if args.method.startswith("r") else 0, tau=spec.tau, i_max=args.imax or spec.i_max,
+                   max_cycles=args.max_cycles, lu_mode=args.lu_mode)
 trace = []
 if os.environ.get("PHASES"):
     import collections
