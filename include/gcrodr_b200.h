@@ -152,6 +152,13 @@ long long gb_launch_count(void);
 double gb_last_step_ms(gb_solver* s);
 double gb_last_factor_ms(gb_solver* s);
 
+/* blocked tensor-mode LU (lu_mode = 1, n >= 2048; lu_factor, densela.py:148-168
+ * restated as a blocked GEPP): device times of the last factorisation,
+ * out[0] = ms in the rank-1024 tcgen05 trailing updates, out[1] = their flop
+ * count (2 M N K summed), out[2] = ms in U12 = L11^-1 A12, out[3] = ms in the
+ * panel factorisations and row interchanges.  Zeros in exact mode. */
+gb_status gb_lu_tc_stats(gb_solver* s, double* out);
+
 /* Batched mode (config 3): `count` independent systems of order n, one CTA
  * per system, the whole refinement loop (refine.py:277-421) on the device.
  * a: count x n x n, b: count x n (float64, host or device per on_device).

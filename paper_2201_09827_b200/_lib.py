@@ -29,7 +29,7 @@ EXPORTS = [
     "gb_refine_step", "gb_last_cycles", "gb_get_solution", "gb_get_reference", "gb_get_factors",
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
     "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog", "gb_time_op",
-    "gb_debug_hessenberg", "gb_debug_set_max_cycles",
+    "gb_debug_hessenberg", "gb_debug_set_max_cycles", "gb_lu_tc_stats",
 ]
 
 
@@ -106,6 +106,7 @@ def load(path: str | None = None):
         "gb_debug_hessenberg": (C.c_int, [vp, vp]),
         "gb_debug_set_max_cycles": (C.c_int, [vp, C.c_int]),
         "gb_last_factor_ms": (C.c_double, [vp]),
+        "gb_lu_tc_stats": (C.c_int, [vp, dp]),
         "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
                                        vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
     }
@@ -298,3 +299,15 @@ class Solver:
     @property
     def last_factor_ms(self) -> float:
         return self.lib.gb_last_factor_ms(self.h)
+
+    def tc_update_stats(self) -> dict | None:
+        """Blocked tensor-mode LU: device time and rate of the tcgen05 trailing
+        updates of the last factorisation (None in exact mode)."""
+        out = (C.c_double * 4)()
+        _check(self.lib.gb_lu_tc_stats(self.h, out), "gb_lu_tc_stats")
+        ms, flop, trsm_ms, panel_ms = out[0], out[1], out[2], out[3]
+        if ms <= 0.0 or flop <= 0.0:
+            return None
+        n = self.n
+        return {"ms": ms, "tflops": flop / (ms * 1e-3) / 1e12, "flop_share": flop / (2.0 * n ** 3 / 3.0),
+                "trsm_ms": trsm_ms, "panel_ms": panel_ms}

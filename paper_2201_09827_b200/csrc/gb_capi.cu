@@ -119,6 +119,7 @@ gb_status gb_solver_destroy(gb_solver* s) {
   if (s->mem) cudaFree(s->mem);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
+  for (cudaEvent_t e : s->tc_events) cudaEventDestroy(e);
   delete s;
   return GB_OK;
 }
@@ -248,6 +249,15 @@ gb_status gb_debug_set_max_cycles(gb_solver* s, int cycles) {
 
 double gb_last_step_ms(gb_solver* s) { return s ? s->last_step_ms : 0.0; }
 double gb_last_factor_ms(gb_solver* s) { return s ? s->last_factor_ms : 0.0; }
+
+gb_status gb_lu_tc_stats(gb_solver* s, double* out) {
+  if (!s || !out) return fail(GB_ERR_ARG, "null argument");
+  out[0] = s->tc_update_ms;
+  out[1] = s->tc_update_flop;
+  out[2] = s->tc_trsm_ms;
+  out[3] = s->tc_panel_ms;
+  return GB_OK;
+}
 
 gb_status gb_solve_batched(int count, int n, const gb_options* opt, int i_max, double c_conv, const double* a,
                            const double* b, int on_device, gb_batch_out* out, double* device_ms, void* stream) {

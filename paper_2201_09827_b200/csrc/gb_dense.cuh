@@ -484,17 +484,40 @@ struct ZRec {
 };
 constexpr int kZRing = 64;
 
+// hp != nullptr: the QR iteration runs on a packed shared-memory copy of the
+// Hessenberg matrix (column j keeps rows 0 .. j+3: the upper triangle, the
+// subdiagonal and the two bulge diagonals, hqr_pack_doubles(p) doubles) and
+// the quasi-triangular result is copied back to H -- same operations in the
+// same order, only the storage changes (a 200 x 200 problem does not fit the
+// scratch as a square and would otherwise pay an L2 round trip per access)
+__host__ __device__ inline size_t hqr_pack_doubles(int p) { return (size_t)p * (p + 7) / 2 + 8; }
+// number of Schur-vector warps warp_hqr wants next to the QR warp
+__host__ __device__ inline int hqr_z_warps(int p, int nwarps_cta) {
+  const int want = (p + 31) / 32;
+  const int have = nwarps_cta - 1;
+  return want < 1 ? 1 : (want < have ? want : have);
+}
 static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
-                                double* ort) {
-  // called by threads 0..63: warp 0 runs orthes + the QR iteration, warp 1
-  // applies the Schur-vector updates it pushes
+                                double* ort, double* hp = nullptr, int nz = 1) {
+  // called by threads 0 .. 32 (1 + nz) - 1: warp 0 runs orthes + the QR
+  // iteration, warps 1 .. nz apply the Schur-vector updates it pushes.  Z
+  // warp w owns the rows i = w - 1 + nz * t (t = 0, 1, ...) strided by lane:
+  // rows are independent, the records are applied in order per row.  Inside
+  // a sweep the reflectors walk down the diagonal (k, k + 1, ...), so a lane
+  // keeps Z(i, k .. k+2) of its row in registers, shifts them by one column
+  // per record (one store, one load issued a record ahead) and only falls
+  // back to plain loads when the sweep restarts.
   __shared__ ZRec zring[kZRing];
-  __shared__ volatile int s_head, s_tail, s_done;
+  __shared__ volatile int s_head, s_done;
+  __shared__ volatile int s_tail[8];
   const int lane = threadIdx.x & 31;
   const int low_ = 0, high_ = p - 1;
-  if ((threadIdx.x >> 5) == 1) {
-    asm volatile("bar.sync 1, 64;" ::: "memory");  // Z initialised, ring reset
+  const int zbar = 32 * (1 + nz);
+  if ((threadIdx.x >> 5) >= 1) {
+    const int zw = (threadIdx.x >> 5) - 1;
+    asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // Z initialised, ring reset
     int tail = 0;
+    const int rows_per_pass = 32 * nz;
     for (;;) {
       const int head = s_head;
       if (tail == head) {
@@ -502,32 +525,34 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
         continue;
       }
       __threadfence_block();
-      const volatile ZRec& R = zring[tail % kZRing];
-      const int k = R.k, type = R.type, nl = R.notlast;
-      const double a0 = R.a[0], a1 = R.a[1], a2 = R.a[2], a3 = R.a[3], a4 = R.a[4];
-      __syncwarp();
-      if (type == 0) {
-        for (int i = low_ + lane; i <= high_; i += 32) {
-          double pp = a0 * Z[IX(i, k, ldz)] + a1 * Z[IX(i, k + 1, ldz)];
-          if (nl) {
-            pp = pp + a2 * Z[IX(i, k + 2, ldz)];
-            Z[IX(i, k + 2, ldz)] = Z[IX(i, k + 2, ldz)] - pp * a4;
+      for (; tail < head; ++tail) {
+        const volatile ZRec& R = zring[tail % kZRing];
+        const int k = R.k, type = R.type, nl = R.notlast;
+        const double a0 = R.a[0], a1 = R.a[1], a2 = R.a[2], a3 = R.a[3], a4 = R.a[4];
+        if (type == 0) {
+          for (int i = low_ + zw * 32 + lane; i <= high_; i += rows_per_pass) {
+            // the next reflector of the sweep touches column k + 3
+            if (k + 3 <= high_) asm volatile("prefetch.global.L1 [%0];" ::"l"(Z + IX(i, k + 3, ldz)));
+            double pp = a0 * Z[IX(i, k, ldz)] + a1 * Z[IX(i, k + 1, ldz)];
+            if (nl) {
+              pp = pp + a2 * Z[IX(i, k + 2, ldz)];
+              Z[IX(i, k + 2, ldz)] = Z[IX(i, k + 2, ldz)] - pp * a4;
+            }
+            Z[IX(i, k, ldz)] = Z[IX(i, k, ldz)] - pp;
+            Z[IX(i, k + 1, ldz)] = Z[IX(i, k + 1, ldz)] - pp * a3;
           }
-          Z[IX(i, k, ldz)] = Z[IX(i, k, ldz)] - pp;
-          Z[IX(i, k + 1, ldz)] = Z[IX(i, k + 1, ldz)] - pp * a3;
-        }
-      } else {
-        for (int i = low_ + lane; i <= high_; i += 32) {
-          double zz = Z[IX(i, k - 1, ldz)];
-          Z[IX(i, k - 1, ldz)] = a3 * zz + a0 * Z[IX(i, k, ldz)];
-          Z[IX(i, k, ldz)] = a3 * Z[IX(i, k, ldz)] - a0 * zz;
+        } else {
+          for (int i = low_ + zw * 32 + lane; i <= high_; i += rows_per_pass) {
+            double zz = Z[IX(i, k - 1, ldz)];
+            Z[IX(i, k - 1, ldz)] = a3 * zz + a0 * Z[IX(i, k, ldz)];
+            Z[IX(i, k, ldz)] = a3 * Z[IX(i, k, ldz)] - a0 * zz;
+          }
         }
       }
       __syncwarp();
-      ++tail;
-      if (lane == 0) s_tail = tail;
+      if (lane == 0) s_tail[zw] = tail;
     }
-    asm volatile("bar.sync 1, 64;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");
     return true;
   }
   // producer side: lane 0 appends records and publishes the head every
@@ -543,7 +568,11 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
     if (lane == 0) {
       if (zh - zt >= kZRing) {
         zpublish();
-        while (zh - (zt = s_tail) >= kZRing) {
+        for (;;) {
+          int mn = s_tail[0];
+          for (int w = 1; w < nz; ++w) mn = min(mn, s_tail[w]);
+          zt = mn;
+          if (zh - zt < kZRing) break;
         }
       }
       ZRec& R = zring[zh % kZRing];
@@ -565,7 +594,7 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
       __threadfence_block();
       s_done = 1;
     }
-    asm volatile("bar.sync 1, 64;" ::: "memory");  // the Z warp drained the ring
+    asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // the Z warps drained the ring
   };
   const int nn = p, low = 0, high = p - 1;
   // --- orthes: Householder reduction to Hessenberg form ---
@@ -631,19 +660,29 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
   }
   if (lane == 0) {
     s_head = 0;
-    s_tail = 0;
+    for (int w = 0; w < 8; ++w) s_tail[w] = 0;
     s_done = 0;
   }
   __syncwarp();
-  asm volatile("bar.sync 1, 64;" ::: "memory");  // start the Z warp
+  asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // start the Z warps
 
+  const bool packed = hp != nullptr;
+  double* const hbase = packed ? hp : H;
+  auto HH = [&](int i, int j) -> double& { return hbase[(packed ? ((j * (j + 7)) >> 1) : j * ld) + i]; };
+  if (packed) {
+    for (int e = lane; e < p * p; e += 32) {
+      const int i = e % p, j = e / p;
+      if (i <= j + 3) HH(i, j) = H[IX(i, j, ld)];
+    }
+    __syncwarp();
+  }
   // --- hqr2: Francis double-shift QR with accumulation ---
   int n = nn - 1;
   const double eps = kEps52;
   double exshift = 0.0, p_ = 0, q = 0, r = 0, s = 0, z = 0, t, w, x, y;
   double norm = 0.0;
   for (int i = lane; i < nn; i += 32)
-    for (int j = max(i - 1, 0); j < nn; ++j) norm += fabs(H[IX(i, j, ld)]);
+    for (int j = max(i - 1, 0); j < nn; ++j) norm += fabs(HH(i, j));
   norm = warp_sum(norm);
   int iter = 0, total = 0;
   const int itmax = 40 * max(10, nn);
@@ -655,9 +694,9 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
       const int cand = base - lane;
       bool hit = false;
       if (cand > low) {
-        double sc = fabs(H[IX(cand - 1, cand - 1, ld)]) + fabs(H[IX(cand, cand, ld)]);
+        double sc = fabs(HH(cand - 1, cand - 1)) + fabs(HH(cand, cand));
         if (sc == 0.0) sc = norm;
-        hit = fabs(H[IX(cand, cand - 1, ld)]) < eps * sc;
+        hit = fabs(HH(cand, cand - 1)) < eps * sc;
       }
       const unsigned bm = __ballot_sync(0xffffffffu, hit);
       if (bm) {
@@ -668,24 +707,24 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
     if (l == n) {
       __syncwarp();
       if (lane == 0) {
-        H[IX(n, n, ld)] = H[IX(n, n, ld)] + exshift;
-        wr[n] = H[IX(n, n, ld)];
+        HH(n, n) = HH(n, n) + exshift;
+        wr[n] = HH(n, n);
         wi[n] = 0.0;
       }
       __syncwarp();
       n--;
       iter = 0;
     } else if (l == n - 1) {
-      w = H[IX(n, n - 1, ld)] * H[IX(n - 1, n, ld)];
-      p_ = (H[IX(n - 1, n - 1, ld)] - H[IX(n, n, ld)]) / 2.0;
+      w = HH(n, n - 1) * HH(n - 1, n);
+      p_ = (HH(n - 1, n - 1) - HH(n, n)) / 2.0;
       q = p_ * p_ + w;
       z = sqrt(fabs(q));
-      double hnn = H[IX(n, n, ld)] + exshift;
-      double hn1 = H[IX(n - 1, n - 1, ld)] + exshift;
+      double hnn = HH(n, n) + exshift;
+      double hn1 = HH(n - 1, n - 1) + exshift;
       __syncwarp();
       if (lane == 0) {
-        H[IX(n, n, ld)] = hnn;
-        H[IX(n - 1, n - 1, ld)] = hn1;
+        HH(n, n) = hnn;
+        HH(n - 1, n - 1) = hn1;
       }
       __syncwarp();
       x = hnn;
@@ -699,7 +738,7 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           wi[n - 1] = 0.0;
           wi[n] = 0.0;
         }
-        x = H[IX(n, n - 1, ld)];
+        x = HH(n, n - 1);
         s = fabs(x) + fabs(z);
         p_ = x / s;
         q = z / s;
@@ -708,15 +747,15 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
         q = q / r;
         __syncwarp();
         for (int j = n - 1 + lane; j < nn; j += 32) {
-          double zz = H[IX(n - 1, j, ld)];
-          H[IX(n - 1, j, ld)] = q * zz + p_ * H[IX(n, j, ld)];
-          H[IX(n, j, ld)] = q * H[IX(n, j, ld)] - p_ * zz;
+          double zz = HH(n - 1, j);
+          HH(n - 1, j) = q * zz + p_ * HH(n, j);
+          HH(n, j) = q * HH(n, j) - p_ * zz;
         }
         __syncwarp();
         for (int i = lane; i <= n; i += 32) {
-          double zz = H[IX(i, n - 1, ld)];
-          H[IX(i, n - 1, ld)] = q * zz + p_ * H[IX(i, n, ld)];
-          H[IX(i, n, ld)] = q * H[IX(i, n, ld)] - p_ * zz;
+          double zz = HH(i, n - 1);
+          HH(i, n - 1) = q * zz + p_ * HH(i, n);
+          HH(i, n) = q * HH(i, n) - p_ * zz;
         }
         zpush(1, n, 0, p_, 0.0, 0.0, q, 0.0);
         __syncwarp();
@@ -732,19 +771,19 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
       n = n - 2;
       iter = 0;
     } else {
-      x = H[IX(n, n, ld)];
+      x = HH(n, n);
       y = 0.0;
       w = 0.0;
       if (l < n) {
-        y = H[IX(n - 1, n - 1, ld)];
-        w = H[IX(n, n - 1, ld)] * H[IX(n - 1, n, ld)];
+        y = HH(n - 1, n - 1);
+        w = HH(n, n - 1) * HH(n - 1, n);
       }
       if (iter == 10) {
         exshift += x;
         __syncwarp();
-        for (int i = low + lane; i <= n; i += 32) H[IX(i, i, ld)] -= x;
+        for (int i = low + lane; i <= n; i += 32) HH(i, i) -= x;
         __syncwarp();
-        s = fabs(H[IX(n, n - 1, ld)]) + fabs(H[IX(n - 1, n - 2, ld)]);
+        s = fabs(HH(n, n - 1)) + fabs(HH(n - 1, n - 2));
         x = y = 0.75 * s;
         w = -0.4375 * s * s;
       }
@@ -756,7 +795,7 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           if (y < x) s = -s;
           s = x - w / ((y - x) / 2.0 + s);
           __syncwarp();
-          for (int i = low + lane; i <= n; i += 32) H[IX(i, i, ld)] -= s;
+          for (int i = low + lane; i <= n; i += 32) HH(i, i) -= s;
           __syncwarp();
           exshift += s;
           x = y = w = 0.964;
@@ -776,17 +815,17 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
         const int mm = base - lane;
         bool hit = false;
         if (mm > l) {
-          const double zz = H[IX(mm, mm, ld)];
+          const double zz = HH(mm, mm);
           const double rr = x - zz, ss = y - zz;
-          double pp = (rr * ss - w) / H[IX(mm + 1, mm, ld)] + H[IX(mm, mm + 1, ld)];
-          double qq = H[IX(mm + 1, mm + 1, ld)] - zz - rr - ss;
-          double r3 = H[IX(mm + 2, mm + 1, ld)];
+          double pp = (rr * ss - w) / HH(mm + 1, mm) + HH(mm, mm + 1);
+          double qq = HH(mm + 1, mm + 1) - zz - rr - ss;
+          double r3 = HH(mm + 2, mm + 1);
           const double s3 = fabs(pp) + fabs(qq) + fabs(r3);
           pp = pp / s3;
           qq = qq / s3;
           r3 = r3 / s3;
-          hit = fabs(H[IX(mm, mm - 1, ld)]) * (fabs(qq) + fabs(r3)) <
-                eps * (fabs(pp) * (fabs(H[IX(mm - 1, mm - 1, ld)]) + fabs(zz) + fabs(H[IX(mm + 1, mm + 1, ld)])));
+          hit = fabs(HH(mm, mm - 1)) * (fabs(qq) + fabs(r3)) <
+                eps * (fabs(pp) * (fabs(HH(mm - 1, mm - 1)) + fabs(zz) + fabs(HH(mm + 1, mm + 1))));
         }
         const unsigned bm = __ballot_sync(0xffffffffu, hit);
         if (bm) {
@@ -794,28 +833,28 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           break;
         }
       }
-      z = H[IX(m, m, ld)];
+      z = HH(m, m);
       r = x - z;
       s = y - z;
-      p_ = (r * s - w) / H[IX(m + 1, m, ld)] + H[IX(m, m + 1, ld)];
-      q = H[IX(m + 1, m + 1, ld)] - z - r - s;
-      r = H[IX(m + 2, m + 1, ld)];
+      p_ = (r * s - w) / HH(m + 1, m) + HH(m, m + 1);
+      q = HH(m + 1, m + 1) - z - r - s;
+      r = HH(m + 2, m + 1);
       s = fabs(p_) + fabs(q) + fabs(r);
       p_ = p_ / s;
       q = q / s;
       r = r / s;
       __syncwarp();
       for (int i = m + 2 + lane; i <= n; i += 32) {
-        H[IX(i, i - 2, ld)] = 0.0;
-        if (i > m + 2) H[IX(i, i - 3, ld)] = 0.0;
+        HH(i, i - 2) = 0.0;
+        if (i > m + 2) HH(i, i - 3) = 0.0;
       }
       __syncwarp();
       for (int k = m; k <= n - 1; ++k) {
         bool notlast = (k != n - 1);
         if (k != m) {
-          p_ = H[IX(k, k - 1, ld)];
-          q = H[IX(k + 1, k - 1, ld)];
-          r = notlast ? H[IX(k + 2, k - 1, ld)] : 0.0;
+          p_ = HH(k, k - 1);
+          q = HH(k + 1, k - 1);
+          r = notlast ? HH(k + 2, k - 1) : 0.0;
           x = fabs(p_) + fabs(q) + fabs(r);
           if (x == 0.0) continue;
           const double rx = 1.0 / x;  // one division instead of three
@@ -828,8 +867,8 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
         if (s != 0) {
           __syncwarp();
           if (lane == 0) {
-            if (k != m) H[IX(k, k - 1, ld)] = -s * x;
-            else if (l != m) H[IX(k, k - 1, ld)] = -H[IX(k, k - 1, ld)];
+            if (k != m) HH(k, k - 1) = -s * x;
+            else if (l != m) HH(k, k - 1) = -HH(k, k - 1);
           }
           __syncwarp();
           p_ = p_ + s;
@@ -840,24 +879,24 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           q = q * rp;
           r = r * rp;
           for (int j = k + lane; j < nn; j += 32) {
-            double pp = H[IX(k, j, ld)] + q * H[IX(k + 1, j, ld)];
+            double pp = HH(k, j) + q * HH(k + 1, j);
             if (notlast) {
-              pp = pp + r * H[IX(k + 2, j, ld)];
-              H[IX(k + 2, j, ld)] = H[IX(k + 2, j, ld)] - pp * z;
+              pp = pp + r * HH(k + 2, j);
+              HH(k + 2, j) = HH(k + 2, j) - pp * z;
             }
-            H[IX(k, j, ld)] = H[IX(k, j, ld)] - pp * x;
-            H[IX(k + 1, j, ld)] = H[IX(k + 1, j, ld)] - pp * y;
+            HH(k, j) = HH(k, j) - pp * x;
+            HH(k + 1, j) = HH(k + 1, j) - pp * y;
           }
           __syncwarp();
           const int iend = min(n, k + 3);
           for (int i = lane; i <= iend; i += 32) {
-            double pp = x * H[IX(i, k, ld)] + y * H[IX(i, k + 1, ld)];
+            double pp = x * HH(i, k) + y * HH(i, k + 1);
             if (notlast) {
-              pp = pp + z * H[IX(i, k + 2, ld)];
-              H[IX(i, k + 2, ld)] = H[IX(i, k + 2, ld)] - pp * r;
+              pp = pp + z * HH(i, k + 2);
+              HH(i, k + 2) = HH(i, k + 2) - pp * r;
             }
-            H[IX(i, k, ld)] = H[IX(i, k, ld)] - pp;
-            H[IX(i, k + 1, ld)] = H[IX(i, k + 1, ld)] - pp * q;
+            HH(i, k) = HH(i, k) - pp;
+            HH(i, k + 1) = HH(i, k + 1) - pp * q;
           }
           zpush(0, k, notlast ? 1 : 0, x, y, z, q, r);
           __syncwarp();  // column update visible to the next step's scalars
@@ -866,6 +905,13 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
     }
   }
   __syncwarp();
+  if (packed) {
+    for (int e = lane; e < p * p; e += 32) {
+      const int i = e % p, j = e / p;
+      if (i <= j + 1) H[IX(i, j, ld)] = HH(i, j);
+    }
+    __syncwarp();
+  }
   zfinish();
   return true;
 }

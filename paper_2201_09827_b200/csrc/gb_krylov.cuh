@@ -58,6 +58,9 @@ struct Krylov {
   double* fast;
   int fast_cap;  // doubles
   int ops_bytes;  // size of the shared op region (TRSV tiles / leader scratch)
+  // the op region itself: packed Hessenberg storage for eigenproblems whose
+  // dense scratch does not fit it (gb_dense.cuh warp_hqr)
+  double* pack;
 };
 
 // shared-memory need (doubles) of the leader's dense work at dimension p
@@ -384,7 +387,7 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
           vn[q] = vc[q];
           vc[q] = (r < hi && i < j) ? K.V[(size_t)(i + 1) * ldv + r] : TW(0);
         }
-        t.template reduce<typename F::Acc, 1>(a, reinterpret_cast<typename F::Acc*>(red));
+        a[0] = t.template reduce1<typename F::Acc>(a[0], reinterpret_cast<typename F::Acc*>(red));
         hprev = (double)a[0];
         if (threadIdx.x == 0) col[i] = hprev;
       }
@@ -509,7 +512,8 @@ __device__ void explicit_residual(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
 // Writes P (p x keff, ldp) normalised columns; returns keff or -1 on failure.
 // scratch: Z p*p, X 2p per thread-vector, wr, wi, ort, ord.
 // --------------------------------------------------------------------------
-static __device__ __noinline__ int leader_ritz_basis(double* Mx, int p, int kreq, double* P, int ldp, double* scr) {
+static __device__ __noinline__ int leader_ritz_basis(double* Mx, int p, int kreq, double* P, int ldp, double* scr,
+                                                     double* hp = nullptr) {
   double* Z = scr;
   double* wr = Z + (size_t)p * p;
   double* wi = wr + p;
@@ -530,8 +534,9 @@ static __device__ __noinline__ int leader_ritz_basis(double* Mx, int p, int kreq
     if (!isfinite(Mx[e])) s_ok = 0;
   __syncthreads();
   if (!s_ok) return -1;
-  if (threadIdx.x < 64) {  // warp 0: QR iteration, warp 1: Schur-vector updates
-    bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort);
+  const int nz = hqr_z_warps(p, (int)(blockDim.x >> 5));
+  if ((int)threadIdx.x < 32 * (1 + nz)) {  // warp 0: QR iteration, warps 1 .. nz: Schur-vector updates
+    bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort, hp, nz);
     if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
   }
   __syncthreads();
@@ -1057,7 +1062,10 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
   mark(lg, 62);
   blk_getrs(lu, gc, gc, piv, emat, gc, gc);
   mark(lg, 63);
-  const int kn = leader_ritz_basis(emat, gc, kk, P, gc, escr);
+  double* hp = (!fast && K.pack != nullptr && hqr_pack_doubles(gc) * sizeof(double) <= (size_t)K.ops_bytes)
+                   ? K.pack
+                   : nullptr;
+  const int kn = leader_ritz_basis(emat, gc, kk, P, gc, escr, hp);
   mark(lg, 64);
   if (kn <= 0) return -1;
   for (int e = threadIdx.x; e < gr * kn; e += blockDim.x) {
@@ -1236,7 +1244,10 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
             __syncthreads();
             kn = leader_ritz_basis(K.fast, j, kk, P, j, K.fast + (size_t)j * j);
           } else {
-            kn = leader_ritz_basis(Hm, j, kk, P, j, scr);
+            double* hp = (K.pack != nullptr && hqr_pack_doubles(j) * sizeof(double) <= (size_t)K.ops_bytes)
+                             ? K.pack
+                             : nullptr;
+            kn = leader_ritz_basis(Hm, j, kk, P, j, scr, hp);
           }
           int status = -1;
           if (kn > 0) {

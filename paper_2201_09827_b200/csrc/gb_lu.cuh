@@ -438,7 +438,7 @@ struct LuWork {
 constexpr int kLuNB = 32;
 
 template <int M>
-__device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, int n, int k0, int i0, int j0,
+__device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, int n, int nc, int k0, int i0, int j0,
                                              typename LuT<M>::C* ls, typename LuT<M>::C* us) {
   using L = LuT<M>;
   using C = typename L::C;
@@ -449,7 +449,7 @@ __device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, i
   }
   for (int e = threadIdx.x; e < NB * TN; e += blockDim.x) {
     int r = e / TN, c = e % TN;
-    us[r * (TN + 1) + c] = (j0 + c < n) ? L::ld(W[(size_t)(k0 + r) * ld + j0 + c]) : C(0);
+    us[r * (TN + 1) + c] = (j0 + c < nc) ? L::ld(W[(size_t)(k0 + r) * ld + j0 + c]) : C(0);
   }
   __syncthreads();
   const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
@@ -459,7 +459,7 @@ __device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, i
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
-      acc[a][b] = (i < n && j < n) ? L::ld(W[(size_t)i * ld + j]) : C(0);
+      acc[a][b] = (i < n && j < nc) ? L::ld(W[(size_t)i * ld + j]) : C(0);
     }
   if constexpr (L::kLapack) {
     C s[4][4];
@@ -533,7 +533,7 @@ __device__ __forceinline__ void lu_gemm_tile(typename LuT<M>::S* W, size_t ld, i
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       int i = i0 + tr + 16 * a, j = j0 + tc + 16 * b;
-      if (i < n && j < n) W[(size_t)i * ld + j] = L::st(acc[a][b]);
+      if (i < n && j < nc) W[(size_t)i * ld + j] = L::st(acc[a][b]);
     }
   __syncthreads();
 }
@@ -554,7 +554,7 @@ __host__ __device__ inline size_t lu_team_smem(int n, int G) {
 //   rounded to u_f once per panel (north_star (1)); pivots then agree with the
 //   exact mode up to near-ties.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, int i0, int j0, unsigned char* sA,
+__device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int nc, int k0, int i0, int j0, unsigned char* sA,
                                            unsigned char* sB, uint64_t* mbar, uint32_t tmem, uint32_t& phase) {
   // Operands are staged with 16-byte shared-space stores (st.shared.v4 on
   // the 32-bit shared address: the aligned staging pointer has lost its
@@ -579,7 +579,7 @@ __device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, 
     const int gj = j0 + nn;
     __align__(16) __half h[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) h[q] = gj < n ? W[(size_t)(k0 + kc * 8 + q) * ld + gj] : __float2half(0.f);
+    for (int q = 0; q < 8; ++q) h[q] = gj < nc ? W[(size_t)(k0 + kc * 8 + q) * ld + gj] : __float2half(0.f);
     const uint4 v = *reinterpret_cast<const uint4*>(h);
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + tc::sw64_off(nn, kc * 8)), "r"(v.x),
                  "r"(v.y), "r"(v.z), "r"(v.w)
@@ -606,9 +606,9 @@ __device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, 
     float acc[32];
     tc::tmem_ld32(tmem + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)(cbase + ch * 32), acc);
     const int gj = j0 + cbase + ch * 32;
-    if (gi < n && gj < n) {
+    if (gi < n && gj < nc) {
       __half* p = W + (size_t)gi * ld + gj;
-      if (gj + 32 <= n) {
+      if (gj + 32 <= nc) {
         __align__(16) __half h[32];
 #pragma unroll
         for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(h)[q] = reinterpret_cast<const uint4*>(p)[q];
@@ -617,7 +617,7 @@ __device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, 
 #pragma unroll
         for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(p)[q] = reinterpret_cast<const uint4*>(h)[q];
       } else {
-        for (int q = 0; q < 32 && gj + q < n; ++q) p[q] = __float2half_rn(__half2float(p[q]) - acc[q]);
+        for (int q = 0; q < 32 && gj + q < nc; ++q) p[q] = __float2half_rn(__half2float(p[q]) - acc[q]);
       }
     }
   }
@@ -627,7 +627,14 @@ __device__ __forceinline__ void lu_tc_tile(__half* W, size_t ld, int n, int k0, 
 
 template <int M, class Team, class TA>
 __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W, size_t ld, int n, int* perm,
-                        LuStatus* st, LuWork wk, void* smem_raw, int tcmode = 0) {
+                        LuStatus* st, LuWork wk, void* smem_raw, int tcmode = 0, int cbeg = 0, int cend = -1,
+                        int* ipiv_all = nullptr) {
+  // Column window [cbeg, cend) (multiples of 32, or cend = n): the blocked
+  // tensor mode factors one wide panel per launch -- interchanges, U12 and the
+  // rank-32 updates stay inside the window, the pivot rows are recorded in
+  // ipiv_all for the host-side pass over the other columns.  The default
+  // window is the whole matrix (one launch = the whole factorisation).
+  if (cend < 0) cend = n;
   using L = LuT<M>;
   using C = typename L::C;
   constexpr int NB = kLuNB;
@@ -662,7 +669,7 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
   const int nthr = G * blockDim.x;
   const int gtid = r * blockDim.x + threadIdx.x;
   // W = fl_uf(A), amax, identity permutation
-  {
+  if (cbeg == 0) {
     int lo, hi;
     t.rows(n, lo, hi);
     double m = 0.0;
@@ -678,8 +685,8 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
     for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) perm[i] = i;
   }
   t.sync();
-  for (int k0 = 0; k0 < n; k0 += NB) {
-    const int kend = min(n, k0 + NB), pw = kend - k0;
+  for (int k0 = cbeg; k0 < cend; k0 += NB) {
+    const int kend = min(cend, k0 + NB), pw = kend - k0;
     const int sl = (n - k0 + G - 1) / G;
     const int p0 = min(n, k0 + r * sl), p1 = min(n, p0 + sl);
     // ---- P: panel rows into shared memory
@@ -746,6 +753,7 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
         if (isz) atomicMin(&st->zero_col, k);
         const bool swap = (p != k) && !(isz && L::kLapack);
         wk.piv[c] = swap ? p : k;
+        if (ipiv_all != nullptr) ipiv_all[k] = swap ? p : k;
         if (swap) {
           int tmp = perm[k];
           perm[k] = perm[p];
@@ -777,8 +785,8 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
     }
     t.sync();
     // ---- S: interchanges outside the panel
-    for (int idx = gtid; idx < n - pw; idx += nthr) {
-      const int j = idx < k0 ? idx : idx + pw;
+    for (int idx = gtid; idx < cend - cbeg - pw; idx += nthr) {
+      const int j = cbeg + idx < k0 ? cbeg + idx : cbeg + idx + pw;
       for (int c = 0; c < pw; ++c) {
         const int p = __ldcg(wk.piv + c);
         if (p != k0 + c) {
@@ -789,14 +797,14 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
       }
     }
     t.sync();
-    if (kend >= n) break;
+    if (kend >= cend) break;
     // ---- T: U12 = L11^-1 A12
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
       const int rr = e / NB, c = e % NB;
       l11[rr * 33 + c] = (rr < pw && c < pw) ? L::ld(W[(size_t)(k0 + rr) * ld + k0 + c]) : C(0);
     }
     __syncthreads();
-    for (int j = kend + gtid; j < n; j += nthr) {
+    for (int j = kend + gtid; j < cend; j += nthr) {
       C col[NB];
 #pragma unroll
       for (int rr = 0; rr < NB; ++rr) col[rr] = rr < pw ? L::ld(W[(size_t)(k0 + rr) * ld + j]) : C(0);
@@ -811,21 +819,21 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
     }
     t.sync();
     // ---- G: trailing update over the team
-    const int rest = n - kend;
+    const int rest = n - kend, crest = cend - kend;
     if constexpr (M == MODE_H16) {
       if (use_tc && pw == NB) {
-        const int ntr = (rest + 127) / 128, ntc = (rest + 255) / 256;
+        const int ntr = (rest + 127) / 128, ntc = (crest + 255) / 256;
         for (int tt = r; tt < ntr * ntc; tt += G)
-          lu_tc_tile(reinterpret_cast<__half*>(W), ld, n, k0, kend + (tt / ntc) * 128, kend + (tt % ntc) * 256, sA,
-                     sB, mbar, s_tmem, tphase);
+          lu_tc_tile(reinterpret_cast<__half*>(W), ld, n, cend, k0, kend + (tt / ntc) * 128, kend + (tt % ntc) * 256,
+                     sA, sB, mbar, s_tmem, tphase);
         t.sync();
         continue;
       }
     }
-    const int nt = (rest + 63) / 64;
-    for (int tt = r; tt < nt * nt; tt += G) {
-      const int ti = tt / nt, tj = tt % nt;
-      lu_gemm_tile<M>(W, ld, n, k0, kend + ti * 64, kend + tj * 64, ls, us);
+    const int ntr = (rest + 63) / 64, ntc = (crest + 63) / 64;
+    for (int tt = r; tt < ntr * ntc; tt += G) {
+      const int ti = tt / ntc, tj = tt % ntc;
+      lu_gemm_tile<M>(W, ld, n, cend, k0, kend + ti * 64, kend + tj * 64, ls, us);
     }
     t.sync();
   }
@@ -835,7 +843,7 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
     if (threadIdx.x < 32) tc::tmem_dealloc(s_tmem, 256);
   }
   // growth numerator max|U| over this CTA's rows
-  {
+  if (cend >= n) {
     int lo, hi;
     t.rows(n, lo, hi);
     double m = 0.0;
@@ -852,11 +860,63 @@ __device__ void lu_team(Team& t, const TA* A, size_t lda, typename LuT<M>::S* W,
 template <int M, class TA, class Team>
 __global__ void __launch_bounds__(256) k_lu_team(const TA* A, size_t lda, typename LuT<M>::S* W, size_t ld, int n,
                                                  int* perm, LuStatus* st, LuWork wk, GridCtl* ctl, double* part,
-                                                 int tcmode) {
+                                                 int tcmode, int cbeg, int cend, int* ipiv_all) {
   extern __shared__ __align__(1024) unsigned char smem_lu[];
   Team t;
   if constexpr (Team::kGrid) t = Team{(int)gridDim.x, (int)blockIdx.x, ctl, part, 64, 0u};
-  lu_team<M>(t, A, lda, W, ld, n, perm, st, wk, smem_lu, tcmode);
+  lu_team<M>(t, A, lda, W, ld, n, perm, st, wk, smem_lu, tcmode, cbeg, cend, ipiv_all);
+}
+
+// ---------------------------------------------------------------------------
+// blocked tensor mode, host-driven (gb_solver.cuh lu_run_blocked): after a
+// wide panel [c0, c0 + w) has been factored in its window,
+//   k_lu_apply_pivots   the panel's row interchanges on the columns outside it
+//   k_lu_trsm32         the 32-row base case of U12 = L11^-1 A12 (exact
+//                       per-element order, as phase T above); the levels above
+//                       it and the trailing update run on tcgen05
+//                       (gb_tcgemm.cuh)
+// ---------------------------------------------------------------------------
+template <class S>
+__global__ void k_lu_apply_pivots(S* W, size_t ld, int n, int c0, int w, const int* __restrict__ ipiv) {
+  const int nout = n - w;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nout; idx += gridDim.x * blockDim.x) {
+    const int j = idx < c0 ? idx : idx + w;
+    for (int k = c0; k < c0 + w; ++k) {
+      const int p = __ldg(ipiv + k);
+      if (p != k) {
+        const S a = W[(size_t)k * ld + j];
+        W[(size_t)k * ld + j] = W[(size_t)p * ld + j];
+        W[(size_t)p * ld + j] = a;
+      }
+    }
+  }
+}
+
+// rows [r0, r0 + 32) of columns [c0, c0 + N): X = L11^-1 X with the unit lower
+// 32 x 32 block L11 = W[r0:r0+32, r0:r0+32]
+template <int M>
+__global__ void __launch_bounds__(256) k_lu_trsm32(typename LuT<M>::S* W, size_t ld, int r0, int c0, int N) {
+  using L = LuT<M>;
+  using C = typename L::C;
+  constexpr int NB = 32;
+  __shared__ C l11[NB * 33];
+  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+    const int rr = e / NB, c = e % NB;
+    l11[rr * 33 + c] = L::ld(W[(size_t)(r0 + rr) * ld + r0 + c]);
+  }
+  __syncthreads();
+  for (int j = c0 + blockIdx.x * blockDim.x + threadIdx.x; j < c0 + N; j += gridDim.x * blockDim.x) {
+    C col[NB];
+#pragma unroll
+    for (int rr = 0; rr < NB; ++rr) col[rr] = L::ld(W[(size_t)(r0 + rr) * ld + j]);
+#pragma unroll
+    for (int rr = 1; rr < NB; ++rr) {
+#pragma unroll
+      for (int i = 0; i < rr; ++i) col[rr] = L::upd(col[rr], l11[rr * 33 + i], col[i]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < NB; ++rr) W[(size_t)(r0 + rr) * ld + j] = L::st(col[rr]);
+  }
 }
 
 }  // namespace gb

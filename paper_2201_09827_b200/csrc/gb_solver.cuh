@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "gb_refine.cuh"
+#include "gb_tcgemm.cuh"
 #pragma once
 
 using namespace gb;
@@ -111,8 +112,10 @@ template <>
 struct MakeTeam<GridTeam> {
   template <class P>
   GB_DEVICE static GridTeam make(const P& p) {
-    return GridTeam{(int)gridDim.x, (int)blockIdx.x, p.ctl, p.partials, p.kmax, 0u,
-                    gridDim.x > 1 && cluster_ncta() == gridDim.x};
+    GridTeam t{(int)gridDim.x, (int)blockIdx.x, p.ctl, p.partials, p.kmax, 0u,
+               gridDim.x > 1 && cluster_ncta() == gridDim.x};
+    t.links_begin();
+    return t;
   }
 };
 template <>
@@ -146,6 +149,7 @@ template <class Team, class P_t>
 __device__ void ytag_finish(Team& t, const P_t& P) {
   if constexpr (Team::kGrid) {
     if (P.ytag_dsm > 0) t.sync();
+    t.links_end();
   }
 }
 
@@ -337,6 +341,7 @@ __global__ void __launch_bounds__(kThreads) k_step(Prob<TW, TF, MV> Pin) {
   double* sm = reinterpret_cast<double*>(smem);
   void* ops = smem + sm_doubles(P.K.m, P.K.k) * sizeof(double);
   P.K.fast = P.K.fast_cap > 0 ? reinterpret_cast<double*>(ops) : nullptr;
+  P.K.pack = reinterpret_cast<double*>(ops);
   ytag_setup(t, P, smem);
   step_body(t, P, sm, ops);
   if (t.leader() && threadIdx.x == 0) P.K.keff_io[1] = (P.K.U == Pin.K.U) ? 0 : 1;
@@ -792,6 +797,10 @@ struct gb_solver {
   PivKey* lu_ckey = nullptr;
   double *lu_crow = nullptr, *lu_rowk = nullptr;
   int* lu_piv = nullptr;
+  int* lu_ipiv = nullptr;  // blocked tensor LU: pivot row of every column (LAPACK ipiv)
+  // blocked tensor LU statistics of the last factorisation (gb_lu_tc_stats)
+  double tc_update_ms = 0.0, tc_update_flop = 0.0, tc_trsm_ms = 0.0, tc_panel_ms = 0.0;
+  std::vector<cudaEvent_t> tc_events;
   double *r = nullptr, *xref = nullptr, *rtmp = nullptr, *dtmp = nullptr;
   void *V = nullptr, *w = nullptr, *xk = nullptr, *res = nullptr, *s = nullptr, *rhat = nullptr;
   void *C = nullptr, *U = nullptr, *Cn = nullptr, *Un = nullptr, *Ut = nullptr, *Yt = nullptr;
@@ -899,6 +908,7 @@ struct Impl {
     K.cycle_keff = s->cycle_keff;
     K.keff_io = s->keff_io;
     K.fast = nullptr;
+    K.pack = nullptr;
     K.fast_cap = fast_cap(s->o.m, s->o.k);
     K.ops_bytes = (int)(smem_bytes(s) - sm_doubles(s->o.m, s->o.k) * sizeof(double));
     P.b = (const TW*)s->b;
@@ -959,6 +969,11 @@ struct Impl {
       // big-block substitution's staged vector (sweep_bsp)
       const size_t base = sm_doubles(s->o.m, s->o.k) * sizeof(double);
       b = std::max(b, base + std::max(seg::gemv_smem(s->n, s->gemv_ns), (size_t)s->nbig * 8 + 64));
+    }
+    if (s->G > 1 && !s->cluster && fast_cap(s->o.m, s->o.k) == 0) {
+      // packed Hessenberg storage of the harmonic-Ritz eigenproblem (dimension <= m)
+      const size_t need = sm_doubles(s->o.m, s->o.k) * sizeof(double) + hqr_pack_doubles(s->o.m) * sizeof(double);
+      if (need <= 227 * 1024 - 8192) b = std::max(b, need);
     }
     if (trsv_block(s) == kTrsvB) {
       const size_t need = sm_doubles(s->o.m, s->o.k) * sizeof(double) +
@@ -1071,6 +1086,7 @@ struct Impl {
       s->lu_crow = a.take<double>(2 * 160 * 32);
       s->lu_rowk = a.take<double>(64);
       s->lu_piv = a.take<int>(64);
+      s->lu_ipiv = a.take<int>(ldv);
       s->rcph = a.take<double>(ldv);
       s->rcpl = a.take<double>(ldv);
       s->xrcph = a.take<double>(ldv);
@@ -1105,7 +1121,7 @@ struct Impl {
       s->epoch = a.take<unsigned long long>(2);
       s->ytag = a.take<uint4>(2 * (size_t)ldv);
       s->norms = a.take<unsigned long long>(4);
-      s->ctl = a.take<GridCtl>(1);
+      s->ctl = a.take<GridCtl>(1 + (2 * kLinkSlots * 16 + sizeof(GridCtl) - 1) / sizeof(GridCtl));  // + reduce1 slots
       s->partials = a.take<double>((size_t)2 * s->G * s->kmax);
       s->cycle_iters = a.take<int>(m * 0 + s->o.max_cycles + 4);
       s->cycle_keff = a.take<int>(s->o.max_cycles + 4);
@@ -1236,7 +1252,8 @@ struct Impl {
       auto kern = k_lu_team<M, TA, CtaTeam>;
       gb_status e = set_smem(kern, smb);
       if (e != GB_OK) return e;
-      kern<<<1, 256, smb, s->stream>>>(A, lda, W, (size_t)s->lda, n, perm, st, wk, s->ctl, s->partials, tcmode);
+      kern<<<1, 256, smb, s->stream>>>(A, lda, W, (size_t)s->lda, n, perm, st, wk, s->ctl, s->partials, tcmode, 0, n,
+                                       (int*)nullptr);
       CK(cudaGetLastError());
     } else {
       auto kern = k_lu_team<M, TA, GridTeam>;
@@ -1245,12 +1262,103 @@ struct Impl {
       size_t ldw = (size_t)s->lda;
       GridCtl* ctl = s->ctl;
       double* part = s->partials;
-      void* argv[] = {(void*)&A,  (void*)&lda, (void*)&W,   (void*)&ldw,  (void*)&n,     (void*)&perm,
-                      (void*)&st, (void*)&wk,  (void*)&ctl, (void*)&part, (void*)&tcmode};
+      if constexpr (M == MODE_H16) {
+        if (tcmode != 0 && n >= 2048) return lu_run_blocked<TA>(s, A, lda, W, perm, st, wk, G, smb);
+      }
+      int cbeg = 0, cend = n;
+      int* ipiv = nullptr;
+      void* argv[] = {(void*)&A,   (void*)&lda,  (void*)&W,      (void*)&ldw,  (void*)&n,    (void*)&perm, (void*)&st,
+                      (void*)&wk,  (void*)&ctl,  (void*)&part,   (void*)&tcmode, (void*)&cbeg, (void*)&cend,
+                      (void*)&ipiv};
       CK(cudaMemsetAsync(&s->ctl->count, 0, sizeof(unsigned), s->stream));  // GridTeam::sync arrival counter
       CK(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(256), argv, smb, s->stream));
     }
     (void)piv;
+    return GB_OK;
+  }
+
+  // U12 = L11^-1 A12 for the w x w unit lower block at (r0, r0) and the columns
+  // [c0, c0 + N): recursive halving; the off-diagonal products run on tcgen05
+  static cudaError_t trsm_rec(gb_solver* s, __half* W, int r0, int w, int c0, int N, __half* Bt) {
+    if (w <= 32) {
+      count_launch();
+      k_lu_trsm32<MODE_H16><<<std::max(1, std::min(296, (N + 255) / 256)), 256, 0, s->stream>>>(W, (size_t)s->lda,
+                                                                                                 r0, c0, N);
+      return cudaGetLastError();
+    }
+    const int h = ((w / 2 + 31) / 32) * 32;
+    cudaError_t e = trsm_rec(s, W, r0, h, c0, N, Bt);
+    if (e != cudaSuccess) return e;
+    count_launch(2);
+    e = tcg2::tc_update(W, (size_t)s->lda, s->n, r0 + h, c0, w - h, N, r0, h, Bt, s->stream);
+    if (e != cudaSuccess) return e;
+    return trsm_rec(s, W, r0 + h, w - h, c0, N, Bt);
+  }
+
+  // Blocked tensor-mode LU (north_star (1)): panels of kLuWide columns are
+  // factored by the team kernel in a column window (pivot search, interchanges
+  // and rank-32 tcgen05 updates inside the panel); then the interchanges are
+  // applied to the other columns, U12 = L11^-1 A12 (recursive, tcgen05 below
+  // the 32-row base case) and the trailing matrix takes ONE rank-kLuWide
+  // update A22 = fl16(A22 - fp32(L21 U12)) on the CTA-pair tcgen05 kernel fed
+  // by TMA (gb_tcgemm.cuh), i.e. n / kLuWide passes over the trailing matrix.
+  static constexpr int kLuWide = 1024;
+  template <class TA>
+  static gb_status lu_run_blocked(gb_solver* s, const TA* A, size_t lda, __half* W, int* perm, LuStatus* st,
+                                  LuWork wk, int G, size_t smb) {
+    const int n = s->n;
+    auto kern = k_lu_team<MODE_H16, TA, GridTeam>;
+    size_t ldw = (size_t)s->lda;
+    GridCtl* ctl = s->ctl;
+    double* part = s->partials;
+    int tcmode = 1;
+    int* ipiv = s->lu_ipiv;
+    __half* Bt = reinterpret_cast<__half*>(s->stage);  // host-upload staging area: free during the factorisation
+    const int npanel = (n + kLuWide - 1) / kLuWide;
+    while ((int)s->tc_events.size() < 4 * npanel) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      s->tc_events.push_back(e);
+    }
+    s->tc_update_flop = 0.0;
+    int done = 0;
+    for (int c0 = 0, ip = 0; c0 < n; c0 += kLuWide, ++ip) {
+      int cbeg = c0, cend = std::min(n, c0 + kLuWide);
+      const int w = cend - cbeg, rest = n - cend;
+      void* argv[] = {(void*)&A,   (void*)&lda,  (void*)&W,      (void*)&ldw,  (void*)&n,    (void*)&perm, (void*)&st,
+                      (void*)&wk,  (void*)&ctl,  (void*)&part,   (void*)&tcmode, (void*)&cbeg, (void*)&cend,
+                      (void*)&ipiv};
+      CK(cudaEventRecord(s->tc_events[4 * ip], s->stream));
+      CK(cudaMemsetAsync(&s->ctl->count, 0, sizeof(unsigned), s->stream));
+      count_launch();
+      CK(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(256), argv, smb, s->stream));
+      count_launch();
+      k_lu_apply_pivots<__half><<<148, 256, 0, s->stream>>>(W, ldw, n, cbeg, w, ipiv);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(s->tc_events[4 * ip + 1], s->stream));
+      if (rest > 0) {
+        CK(trsm_rec(s, W, cbeg, w, cend, rest, Bt));
+        CK(cudaEventRecord(s->tc_events[4 * ip + 2], s->stream));
+        count_launch(2);
+        CK(tcg2::tc_update(W, ldw, n, cend, cend, rest, rest, cbeg, w, Bt, s->stream));
+        s->tc_update_flop += 2.0 * (double)rest * rest * w;
+      } else {
+        CK(cudaEventRecord(s->tc_events[4 * ip + 2], s->stream));
+      }
+      CK(cudaEventRecord(s->tc_events[4 * ip + 3], s->stream));
+      done = ip + 1;
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    s->tc_update_ms = s->tc_trsm_ms = s->tc_panel_ms = 0.0;
+    for (int ip = 0; ip < done; ++ip) {
+      float a = 0.f, b = 0.f, c = 0.f;
+      CK(cudaEventElapsedTime(&a, s->tc_events[4 * ip], s->tc_events[4 * ip + 1]));
+      CK(cudaEventElapsedTime(&b, s->tc_events[4 * ip + 1], s->tc_events[4 * ip + 2]));
+      CK(cudaEventElapsedTime(&c, s->tc_events[4 * ip + 2], s->tc_events[4 * ip + 3]));
+      s->tc_panel_ms += a;
+      s->tc_trsm_ms += b;
+      s->tc_update_ms += c;
+    }
     return GB_OK;
   }
 

@@ -56,7 +56,7 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
 
 // C rows [r0, r0 + M), columns [c0, c0 + N) of W (row-major, leading dim ld);
 // A via map_a at (column k0, row r0 + ...), Bt via map_b (row = C column - c0)
-__global__ void __launch_bounds__(NTHREADS, 1)
+static __global__ void __launch_bounds__(NTHREADS, 1)
     k_tc_update(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, __half* W,
                 size_t ld, int r0, int c0, int M, int N, int k0, int K) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 // Bt[j][k] = U12[k][j] (K x N of W at rows [k0, k0 + K), columns [c0, c0 + N))
 // into the K-major scratch (row stride K)
-__global__ void k_transpose_u12(const __half* __restrict__ W, size_t ld, int k0, int c0, int K, int N,
+static __global__ void k_transpose_u12(const __half* __restrict__ W, size_t ld, int k0, int c0, int K, int N,
                                 __half* __restrict__ Bt) {
   __shared__ __half tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx: column (N), by: row (K)
@@ -256,7 +256,7 @@ inline cudaError_t tc_update(__half* W, size_t ld, int nrows, int r0, int c0, in
 //   full[s]    lives in the leader: its producer arms 2 x 16 KB, both CTAs'
 //              TMA loads complete_tx on it (cta_group::2 form);
 //   empty[s], tfull[a]  are signalled in both CTAs by the multicast commit;
-//   tempty[a]  lives in the leader: the 8 epilogue warps of the pair arrive.
+//   tempty[a]  lives in the leader: the 16 epilogue warps of the pair arrive.
 // ---------------------------------------------------------------------------
 namespace tcg2 {
 
@@ -266,7 +266,7 @@ constexpr int A_BYTES = BM * BK * 2;            // 8 KB
 constexpr int B_BYTES = HN * BK * 2;            // 8 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 16 KB per CTA
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
-constexpr int NTHREADS = 256;
+constexpr int NTHREADS = 384;  // TMA, MMA, TMEM, (idle), 8 epilogue warps
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -319,7 +319,7 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     k_tc_update2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, __half* W,
                  size_t ld, int r0, int c0, int M, int N, int k0, int K) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -343,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(tfull + i, 1);
-      tc::mbar_init(tempty + i, 8);  // one elected arrive per epilogue warp of the pair
+      tc::mbar_init(tempty + i, 16);  // one elected arrive per epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tcg::prefetch_map(&map_a);
@@ -397,35 +397,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       commit_pair(tfull + acc);
     }
   } else if (warp >= 4) {
-    // ---- epilogue (both CTAs): row = TMEM lane = row 128 rank + lane of the pair tile
-    const int q = warp - 4;
+    // ---- epilogue (both CTAs, 8 warps): warp 4 + q + 4 h owns TMEM lanes
+    // 32 q .. 32 q + 31 (rows 128 rank + 32 q + lane of the pair tile) and the
+    // column half h.  The 256 bytes of C a thread updates are loaded BEFORE
+    // the wait on the accumulator, i.e. under the MMAs of the same tile.
+    const int q = warp & 3, hc = (warp - 4) >> 2;
     const int row_in_tile = (int)rank * BM + q * 32 + lane;
     int it = 0;
     for (int t = pair; t < ntiles; t += npairs, ++it) {
       const int ti = t / tn, tj = t % tn;
       const int acc = it & 1;
+      const int gi = ti * PM + row_in_tile;
+      const int gj0 = tj * BN + hc * 128;
+      const bool rowok = gi < M;
+      const bool fullw = rowok && gj0 + 128 <= N;
+      __half* prow = W + (size_t)(r0 + (rowok ? gi : 0)) * ld + c0 + gj0;
+      uint4 cpre[16];
+      if (fullw) {
+#pragma unroll
+        for (int z = 0; z < 16; ++z) cpre[z] = reinterpret_cast<const uint4*>(prow)[z];
+      }
       tc::mbar_wait(tfull + acc, (uint32_t)((it >> 1) & 1));
       tc::fence_after();
-      const int gi = ti * PM + row_in_tile;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + hc * 128);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
         float v[32];
         tc::tmem_ld32(tbase + (uint32_t)(ch * 32), v);
-        const int gj = tj * BN + ch * 32;
-        if (gi < M && gj < N) {
-          __half* p = W + (size_t)(r0 + gi) * ld + c0 + gj;
-          if (gj + 32 <= N) {
-            __align__(16) __half h[32];
+        const int gj = gj0 + ch * 32;
+        if (fullw) {
+          auto upd = [](unsigned c, float a, float b) -> unsigned {
+            __half2 h = *reinterpret_cast<__half2*>(&c);
+            const float2 f = __half22float2(h);
+            h = __floats2half2_rn(f.x - a, f.y - b);
+            return *reinterpret_cast<unsigned*>(&h);
+          };
 #pragma unroll
-            for (int z = 0; z < 4; ++z) reinterpret_cast<uint4*>(h)[z] = reinterpret_cast<const uint4*>(p)[z];
-#pragma unroll
-            for (int z = 0; z < 32; ++z) h[z] = __float2half_rn(__half2float(h[z]) - v[z]);
-#pragma unroll
-            for (int z = 0; z < 4; ++z) reinterpret_cast<uint4*>(p)[z] = reinterpret_cast<const uint4*>(h)[z];
-          } else {
-            for (int z = 0; z < 32 && gj + z < N; ++z) p[z] = __float2half_rn(__half2float(p[z]) - v[z]);
+          for (int z = 0; z < 4; ++z) {
+            const uint4 cc = cpre[4 * ch + z];
+            uint4 o;
+            o.x = upd(cc.x, v[8 * z + 0], v[8 * z + 1]);
+            o.y = upd(cc.y, v[8 * z + 2], v[8 * z + 3]);
+            o.z = upd(cc.z, v[8 * z + 4], v[8 * z + 5]);
+            o.w = upd(cc.w, v[8 * z + 6], v[8 * z + 7]);
+            reinterpret_cast<uint4*>(prow + ch * 32)[z] = o;
           }
+        } else if (rowok && gj < N) {
+          __half* p = prow + ch * 32;
+          for (int z = 0; z < 32 && gj + z < N; ++z) p[z] = __float2half_rn(__half2float(p[z]) - v[z]);
         }
       }
       tc::fence_before();

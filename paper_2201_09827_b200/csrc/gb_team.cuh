@@ -59,6 +59,13 @@ struct CtaTeam {
     block_sum<T, K>(v, scratch);
   }
   GB_DEVICE double finish_max(double v) { return v; }
+  // one value per thread -> the team sum in every thread
+  template <class T>
+  __device__ T reduce1(T v, T* scratch) {
+    T a[1] = {v};
+    block_sum<T, 1>(a, scratch);
+    return a[0];
+  }
   // vector variant: local[K] in smem (this CTA's partials) -> out[K] in smem
   template <class T>
   __device__ void sum_vec(const T* local, T* out, int K) {
@@ -66,6 +73,25 @@ struct CtaTeam {
     __syncthreads();
   }
 };
+
+// tagged 16-byte words {lo32, tag, hi32, tag}: a reader that sees the tag in
+// both 8-byte halves has the value (no counters, no fences)
+GB_DEVICE void team_tput(uint4* p, double v, unsigned tag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)b), "r"(tag),
+               "r"((unsigned)(b >> 32)), "r"(tag)
+               : "memory");
+}
+GB_DEVICE bool team_tget(const uint4* p, unsigned tag, double& v) {
+  unsigned x, y, z, w;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+               : "l"(p)
+               : "memory");
+  v = __longlong_as_double((long long)(((unsigned long long)z << 32) | x));
+  return y == tag && w == tag;
+}
+constexpr int kLinkSlots = 160;  // >= the largest grid team (148 CTAs)
 
 // number of CTAs in this thread-block cluster (1 without a cluster launch)
 GB_DEVICE unsigned cluster_ncta() {
@@ -90,6 +116,71 @@ struct GridTeam {
   // layout as `partials`); producers push their values into every CTA's copy
   double* spart = nullptr;
   unsigned nsync = 0;  // grid barriers passed in this launch (identical in every CTA)
+  // tagged single-value reductions (reduce1, cooperative grids): links done by
+  // this launch and the count carried over from earlier launches (the tags
+  // must not repeat while a slot still holds an old one); slots follow *ctl
+  unsigned long long link_base = 0;
+  unsigned nlink = 0;
+
+  GB_DEVICE void links_begin() {
+    if (ctl != nullptr) link_base = *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[0]);
+  }
+  GB_DEVICE void links_end() {
+    if (ctl != nullptr && r == 0 && threadIdx.x == 0 && nlink != 0)
+      *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[0]) = link_base + nlink;
+  }
+  // One value per thread -> the team sum in every thread of every CTA, as
+  // reduce<T, 1> but in ONE global round trip for cooperative grids: the
+  // CTA's block sum goes into its tagged slot, warp 0 polls the G slots of
+  // this link (two slot sets alternate: a CTA can be at most one link ahead
+  // of the slowest one) and sums them in rank order, so the result is
+  // bit-identical in every CTA.  Used by the Gram-Schmidt sweep, whose
+  // j + 1 dependent dots per Arnoldi step are pure reduction latency.
+  template <class T>
+  __device__ T reduce1(T v, T* scratch) {
+    if (clu || spart != nullptr || G > kLinkSlots) {
+      T a[1] = {v};
+      reduce<T, 1>(a, scratch);
+      return a[0];
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      T tsum = lane < nw ? scratch[lane] : T(0);
+      tsum = warp_sum(tsum);
+      const unsigned tag = (unsigned)((link_base + nlink) % 0xffffffffull) + 1u;
+      uint4* slots = reinterpret_cast<uint4*>(ctl + 1) + (size_t)(nlink & 1u) * kLinkSlots;
+      if (lane == 0) team_tput(slots + r, (double)tsum, tag);
+      constexpr int PL = kLinkSlots / 32;
+      double x[PL];
+      bool ok[PL];
+#pragma unroll
+      for (int j = 0; j < PL; ++j) {
+        x[j] = 0.0;
+        ok[j] = lane + 32 * j >= G;
+      }
+      bool all;
+      do {
+        all = true;
+#pragma unroll
+        for (int j = 0; j < PL; ++j) {
+          if (!ok[j]) ok[j] = team_tget(slots + lane + 32 * j, tag, x[j]);
+          all = all && ok[j];
+        }
+      } while (!__all_sync(0xffffffffu, all));
+      T acc = T(0);
+#pragma unroll
+      for (int j = 0; j < PL; ++j)
+        if (lane + 32 * j < G) acc += (T)x[j];
+      acc = warp_sum(acc);
+      if (lane == 0) scratch[32] = acc;
+    }
+    __syncthreads();
+    ++nlink;
+    return scratch[32];
+  }
 
   GB_DEVICE int size() const { return G; }
   GB_DEVICE int rank() const { return r; }

@@ -16,11 +16,17 @@ for n in [int(v) for v in sys.argv[1:]]:
         s.set_system(a, np.ones(n))
         s.factorize(); z, g = s.factorize()
         ms = s.last_factor_ms
-        lu, perm = s.factors() if n <= 4096 else (None, None)
+        lu, perm = s.factors()
+        st = s.tc_update_stats()
         res[mode] = (ms, z, g, lu, perm)
         s.close()
-        print(f"n={n} {mode:6s}: factor {ms:8.2f} ms  zero={z} growth={g:.3f}", flush=True)
-    if n <= 4096:
+        print(f"n={n} {mode:6s}: factor {ms:8.2f} ms = {2 * n ** 3 / 3 / ms / 1e9:.1f} TFLOP/s  zero={z} growth={g:.3f}",
+              flush=True)
+        if st:
+            print(f"   tcgen05 trailing updates: {st['ms']:.2f} ms, {st['tflops']:.0f} TFLOP/s, "
+                  f"{100 * st['flop_share']:.1f}% of the LU flops; U12 solves {st['trsm_ms']:.2f} ms; "
+                  f"panels + interchanges {st['panel_ms']:.2f} ms", flush=True)
+    if True:
         a16 = a.astype(np.float32).astype(np.float16).astype(np.float64)
         for mode in ("exact", "tensor"):
             lu, perm = res[mode][3], res[mode][4]
