@@ -122,6 +122,23 @@ gb_status gb_precond_rhs(gb_solver* s, const double* r, double* out, int fmt);
 gb_status gb_residual(gb_solver* s, const double* x, double* r, int fmt);
 gb_status gb_lu_solve(gb_solver* s, const double* b, double* x);
 
+/* The inner solver alone, as the refinement loop calls it: gmres_solve
+ * (gmres.py:235-311) for the GMRES methods, gcrodr_solve (gcrodr.py:221-419)
+ * for the recycling ones, on the right-hand side r (rounded to u; the loop
+ * passes fl_u(r / ||r||_inf), refine.py:366-378) with this solver's m, k,
+ * tau, max_cycles.  d = the solution of U^-1 L^-1 A d = U^-1 L^-1 r, info =
+ * iterations / cycles / status / applies / k_eff (per-cycle counts through
+ * gb_last_cycles).  The recycle space is the context's: it is carried from
+ * the previous step or inner solve (recycle_in) and kept for the next one
+ * (the returned RecycleSpace); reset_recycle = 1 starts cold (recycle_in =
+ * None). */
+gb_status gb_debug_inner_solve(gb_solver* s, const double* r, int reset_recycle, double* d, gb_step_info* info);
+
+/* check_convergence's device part (refine.py:194-208): r = b - A x at u_r
+ * (r may be NULL), nbe = ||r||_inf / (||A||_inf ||x||_inf + ||b||_inf), cbe =
+ * max_i |r_i| / (|A| |x| + |b|)_i over the finite ratios. */
+gb_status gb_backward_errors(gb_solver* s, const double* x, double* r, double* nbe, double* cbe);
+
 /* measurement: device time (ms) of one kernel-level launch of `what`
  * (0 apply_preconditioned, 1 precond_rhs, 2 residual in u_r, 3 lu_solve),
  * averaged over `reps` back-to-back launches on device-resident data (the

@@ -11,12 +11,14 @@ from .precision import (Format, PrecisionTriple, half_flushes_subnormals, set_ha
                         squared_format)
 from . import densela, mtx
 from .batched import solve_batched
+from .krylov import GcrodrConfig, GmresConfig, GmresOutcome, RecycleSpace, gcrodr_solve, gmres_solve
 from .refine import (
     ConvergenceDecision,
     DivergenceReason,
     Method,
     RefineConfig,
     RefinementReport,
+    check_convergence,
     classify,
     gmres_ir,
     rgmres_ir,
@@ -38,6 +40,14 @@ __all__ = [
     "RefinementReport",
     "ConvergenceDecision",
     "classify",
+    "check_convergence",
+    "GmresConfig",
+    "GmresOutcome",
+    "gmres_solve",
+    "GcrodrConfig",
+    "RecycleSpace",
+    "gcrodr_solve",
+    "solve_batched",
     "solve",
     "sir",
     "gmres_ir",

@@ -30,6 +30,7 @@ EXPORTS = [
     "gb_apply_preconditioned", "gb_precond_rhs", "gb_residual", "gb_lu_solve",
     "gb_last_step_ms", "gb_last_factor_ms", "gb_solve_batched", "gb_debug_phaselog", "gb_time_op",
     "gb_debug_hessenberg", "gb_debug_set_max_cycles", "gb_lu_tc_stats",
+    "gb_debug_inner_solve", "gb_backward_errors",
 ]
 
 
@@ -107,6 +108,8 @@ def load(path: str | None = None):
         "gb_debug_set_max_cycles": (C.c_int, [vp, C.c_int]),
         "gb_last_factor_ms": (C.c_double, [vp]),
         "gb_lu_tc_stats": (C.c_int, [vp, dp]),
+        "gb_debug_inner_solve": (C.c_int, [vp, vp, C.c_int, vp, C.POINTER(StepInfo)]),
+        "gb_backward_errors": (C.c_int, [vp, vp, vp, dp, dp]),
         "gb_solve_batched": (C.c_int, [C.c_int, C.c_int, C.POINTER(Options), C.c_int, C.c_double,
                                        vp, vp, C.c_int, C.POINTER(BatchOut), dp, vp]),
     }
@@ -311,3 +314,22 @@ class Solver:
         n = self.n
         return {"ms": ms, "tflops": flop / (ms * 1e-3) / 1e12, "flop_share": flop / (2.0 * n ** 3 / 3.0),
                 "trsm_ms": trsm_ms, "panel_ms": panel_ms}
+
+    def inner_solve(self, r: np.ndarray, reset_recycle: bool = False):
+        """gmres_solve / gcrodr_solve on r with this context's m, k, tau
+        (gb_debug_inner_solve): (d, StepInfo)."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        d = np.empty(self.n)
+        info = StepInfo()
+        _check(self.lib.gb_debug_inner_solve(self.h, _ptr(r), int(bool(reset_recycle)), _ptr(d), C.byref(info)),
+               "gb_debug_inner_solve")
+        return d, info
+
+    def backward_errors(self, x: np.ndarray):
+        """(r, nbe, cbe) of check_convergence for x (gb_backward_errors)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        r = np.empty(self.n)
+        nbe, cbe = C.c_double(), C.c_double()
+        _check(self.lib.gb_backward_errors(self.h, _ptr(x), _ptr(r), C.byref(nbe), C.byref(cbe)),
+               "gb_backward_errors")
+        return r, nbe.value, cbe.value

@@ -204,6 +204,41 @@ gb_status gb_residual(gb_solver* s, const double* x, double* r, int fmt) {
   if (!s || !s->have_system) return fail(GB_ERR_STATE, "gb_set_system first");
   return s->ops->debug(s, x, r, 2, fmt);
 }
+gb_status gb_debug_inner_solve(gb_solver* s, const double* r, int reset_recycle, double* d, gb_step_info* info) {
+  if (!s || !r || !d || !info) return fail(GB_ERR_ARG, "null argument");
+  if (!s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
+  if (reset_recycle) {
+    CK(cudaMemsetAsync(s->keff_io, 0, 4 * sizeof(int), s->stream));
+    s->parity = 0;
+  }
+  CK(cudaMemcpyAsync(s->rtmp, r, sizeof(double) * s->n, cudaMemcpyHostToDevice, s->stream));
+  s->inner_only = 1;
+  gb_status e = s->ops->step(s, info);
+  s->inner_only = 0;
+  if (e != GB_OK) return e;
+  CK(cudaMemcpyAsync(d, s->dtmp, sizeof(double) * s->n, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return GB_OK;
+}
+
+gb_status gb_backward_errors(gb_solver* s, const double* x, double* r, double* nbe, double* cbe) {
+  if (!s || !x || !nbe || !cbe) return fail(GB_ERR_ARG, "null argument");
+  if (!s->have_system) return fail(GB_ERR_STATE, "gb_set_system first");
+  std::vector<double> tmp;
+  if (!r) {
+    tmp.resize(s->n);
+    r = tmp.data();
+  }
+  gb_status e = s->ops->debug(s, x, r, 5, s->o.ur);
+  if (e != GB_OK) return e;
+  gb_step_info inf;
+  CK(cudaMemcpyAsync(&inf, s->out, sizeof(inf), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  *nbe = inf.nbe;
+  *cbe = inf.cbe;
+  return GB_OK;
+}
+
 gb_status gb_lu_solve(gb_solver* s, const double* b, double* x) {
   if (!s || !s->have_lu) return fail(GB_ERR_STATE, "gb_factorize first");
   return s->ops->debug(s, b, x, 3, s->o.uf);
@@ -217,16 +252,37 @@ gb_status gb_time_op(gb_solver* s, int what, int reps, double* ms_per_launch) {
 
 gb_status gb_debug_phaselog(gb_solver* s, int cap, unsigned long long* out) {
   if (!s) return fail(GB_ERR_ARG, "null solver");
+  // GB_PLOG_HOST=1: the log lives in mapped pinned host memory, so the marks
+  // written before a faulting launch can still be read afterwards
+  const char* hostenv = std::getenv("GB_PLOG_HOST");
+  const bool want_host = hostenv && hostenv[0] == '1';
+  const size_t words = 1 + 2 * (size_t)s->plog_cap + (s->plog_host ? 256 : 0);  // host mode: + per-CTA last marks
   if (out != nullptr && s->plog != nullptr) {
-    CK(cudaStreamSynchronize(s->stream));
-    CK(cudaMemcpy(out, s->plog, sizeof(unsigned long long) * (1 + 2 * (size_t)s->plog_cap), cudaMemcpyDeviceToHost));
+    if (s->plog_host) {
+      cudaStreamSynchronize(s->stream);  // may fail after a fault: the host copy is still readable
+      cudaGetLastError();
+      memcpy(out, s->plog, sizeof(unsigned long long) * words);
+    } else {
+      CK(cudaStreamSynchronize(s->stream));
+      CK(cudaMemcpy(out, s->plog, sizeof(unsigned long long) * words, cudaMemcpyDeviceToHost));
+    }
   }
-  if (s->plog) cudaFree(s->plog);
+  if (s->plog) {
+    if (s->plog_host) cudaFreeHost(s->plog);
+    else cudaFree(s->plog);
+  }
   s->plog = nullptr;
   s->plog_cap = 0;
   if (cap > 0) {
-    CK(cudaMalloc(&s->plog, sizeof(unsigned long long) * (1 + 2 * (size_t)cap)));
-    CK(cudaMemset(s->plog, 0, sizeof(unsigned long long) * (1 + 2 * (size_t)cap)));
+    const size_t bytes = sizeof(unsigned long long) * (1 + 2 * (size_t)cap + (want_host ? 256 : 0));
+    if (want_host) {
+      CK(cudaHostAlloc(&s->plog, bytes, cudaHostAllocMapped));
+      memset(s->plog, 0, bytes);
+    } else {
+      CK(cudaMalloc(&s->plog, bytes));
+      CK(cudaMemset(s->plog, 0, bytes));
+    }
+    s->plog_host = want_host;
     s->plog_cap = cap;
   }
   return GB_OK;

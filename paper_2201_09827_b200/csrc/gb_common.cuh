@@ -37,6 +37,8 @@ __host__ __device__ constexpr int inv_stride() { return 2 * B * B; }
 struct PhaseLog {
   unsigned long long* buf;
   int cap;
+  // post-mortem mode (host-mapped log): last[b] = (count << 32 | tag) of CTA b's latest mark
+  unsigned long long* last = nullptr;
 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -44,6 +46,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ __forceinline__ void mark(const PhaseLog& L, int tag) {
+  if (L.last != nullptr && threadIdx.x == 0 && blockIdx.x < 256) {
+    const unsigned long long prev = L.last[blockIdx.x];
+    L.last[blockIdx.x] = ((prev >> 32) + 1ull) << 32 | (unsigned long long)(unsigned)tag;
+  }
   if (L.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long i = L.buf[0];
     if ((int)i < L.cap) {

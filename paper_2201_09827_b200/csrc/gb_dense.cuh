@@ -491,6 +491,120 @@ constexpr int kZRing = 64;
 // same order, only the storage changes (a 200 x 200 problem does not fit the
 // scratch as a square and would otherwise pay an L2 round trip per access)
 __host__ __device__ inline size_t hqr_pack_doubles(int p) { return (size_t)p * (p + 7) / 2 + 8; }
+// Householder reduction to Hessenberg form and the accumulated transformation
+// (EISPACK orthes + ortran) by the whole CTA: one thread per column (row) of
+// the two-sided update, every element with exactly the operation order of
+// the one-warp version inside warp_hqr (so the results are bit-identical);
+// the loads of a pass are issued in batches ahead of the stores.  At p = 200
+// the one-warp version costs ~85 ms of L2 round trips per eigenproblem.
+// ort: p doubles of scratch (global or shared); all threads call.
+static __device__ __noinline__ void blk_orthes(double* H, int ld, int p, double* Z, int ldz, double* ort) {
+  const int nn = p, low = 0, high = p - 1;
+  __shared__ double s_sc[34];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  for (int m = low + 1; m <= high - 1; ++m) {
+    // scale = sum_i |H(i, m-1)|, hh = sum_i (H(i, m-1) / scale)^2 in the one-warp order (lane-strided partials,
+    // butterfly): warp 0 computes them
+    if (wid == 0) {
+      double scale = 0.0;
+      for (int i = m + lane; i <= high; i += 32) scale += fabs(H[IX(i, m - 1, ld)]);
+      scale = warp_sum(scale);
+      double hh = 0.0;
+      if (scale != 0.0) {
+        for (int i = m + lane; i <= high; i += 32) {
+          double o = H[IX(i, m - 1, ld)] / scale;
+          ort[i] = o;
+          hh = __fma_rn(o, o, hh);
+        }
+        hh = warp_sum(hh);
+        __syncwarp();
+        double om = ort[m];
+        double g = sqrt(hh);
+        if (om > 0) g = -g;
+        hh = hh - om * g;
+        __syncwarp();
+        if (lane == 0) {
+          ort[m] = om - g;
+          s_sc[2] = g;
+        }
+      }
+      if (lane == 0) {
+        s_sc[0] = scale;
+        s_sc[1] = hh;
+      }
+    }
+    __syncthreads();
+    const double scale = s_sc[0], hh = s_sc[1];
+    if (scale == 0.0) {
+      __syncthreads();
+      continue;
+    }
+    // columns j >= m: H(m.., j) -= f ort, f = (sum_{i = high..m} ort_i H(i, j)) / hh
+    for (int j = m + tid; j < nn; j += nt) {
+      double f = 0.0;
+      for (int i = high; i >= m; --i) f = __fma_rn(ort[i], H[IX(i, j, ld)], f);
+      f = f / hh;
+      for (int i0 = m; i0 <= high; i0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u <= high ? H[IX(i0 + u, j, ld)] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u <= high) H[IX(i0 + u, j, ld)] = __fma_rn(-f, ort[i0 + u], v[u]);
+      }
+    }
+    __syncthreads();
+    // rows i: H(i, m..) -= f ort^T, f = (sum_{j = high..m} ort_j H(i, j)) / hh
+    for (int i = tid; i <= high; i += nt) {
+      double f = 0.0;
+      for (int j = high; j >= m; --j) f = __fma_rn(ort[j], H[IX(i, j, ld)], f);
+      f = f / hh;
+      for (int j0 = m; j0 <= high; j0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = j0 + u <= high ? H[IX(i, j0 + u, ld)] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u <= high) H[IX(i, j0 + u, ld)] = __fma_rn(-f, ort[j0 + u], v[u]);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ort[m] = scale * ort[m];
+      H[IX(m, m - 1, ld)] = scale * s_sc[2];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nn * nn; e += nt) Z[IX(e % nn, e / nn, ldz)] = (e % nn == e / nn) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int m = high - 1; m >= low + 1; --m) {
+    const double hm = H[IX(m, m - 1, ld)];
+    if (hm == 0.0) continue;  // uniform: every thread reads the same entry
+    for (int i = m + 1 + tid; i <= high; i += nt) ort[i] = H[IX(i, m - 1, ld)];
+    __syncthreads();
+    for (int j = m + tid; j <= high; j += nt) {
+      double g = 0.0;
+      for (int i = m; i <= high; ++i) g = __fma_rn(ort[i], Z[IX(i, j, ldz)], g);
+      g = (g / ort[m]) / hm;
+      for (int i0 = m; i0 <= high; i0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u <= high ? Z[IX(i0 + u, j, ldz)] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u <= high) Z[IX(i0 + u, j, ldz)] = __fma_rn(g, ort[i0 + u], v[u]);
+      }
+    }
+    __syncthreads();
+  }
+  // clear below the subdiagonal
+  for (int e = tid; e < nn * nn; e += nt) {
+    int i = e % nn, j = e / nn;
+    if (i > j + 1) H[IX(i, j, ld)] = 0.0;
+  }
+  __syncthreads();
+}
+
 // number of Schur-vector warps warp_hqr wants next to the QR warp
 __host__ __device__ inline int hqr_z_warps(int p, int nwarps_cta) {
   const int want = (p + 31) / 32;
@@ -498,7 +612,7 @@ __host__ __device__ inline int hqr_z_warps(int p, int nwarps_cta) {
   return want < 1 ? 1 : (want < have ? want : have);
 }
 static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
-                                double* ort, double* hp = nullptr, int nz = 1) {
+                                double* ort, double* hp = nullptr, int nz = 1, bool reduced = false) {
   // called by threads 0 .. 32 (1 + nz) - 1: warp 0 runs orthes + the QR
   // iteration, warps 1 .. nz apply the Schur-vector updates it pushes.  Z
   // warp w owns the rows i = w - 1 + nz * t (t = 0, 1, ...) strided by lane:
@@ -597,8 +711,9 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
     asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // the Z warps drained the ring
   };
   const int nn = p, low = 0, high = p - 1;
-  // --- orthes: Householder reduction to Hessenberg form ---
-  for (int m = low + 1; m <= high - 1; ++m) {
+  // --- orthes: Householder reduction to Hessenberg form (skipped when the
+  // CTA has already run blk_orthes) ---
+  for (int m = low + 1; !reduced && m <= high - 1; ++m) {
     double scale = 0.0;
     for (int i = m + lane; i <= high; i += 32) scale += fabs(H[IX(i, m - 1, ld)]);
     scale = warp_sum(scale);
@@ -638,9 +753,9 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
     }
     __syncwarp();
   }
-  for (int e = lane; e < nn * nn; e += 32) Z[IX(e % nn, e / nn, ldz)] = (e % nn == e / nn) ? 1.0 : 0.0;
+  for (int e = lane; !reduced && e < nn * nn; e += 32) Z[IX(e % nn, e / nn, ldz)] = (e % nn == e / nn) ? 1.0 : 0.0;
   __syncwarp();
-  for (int m = high - 1; m >= low + 1; --m) {
+  for (int m = high - 1; !reduced && m >= low + 1; --m) {
     double hm = H[IX(m, m - 1, ld)];
     if (hm == 0.0) continue;
     for (int i = m + 1 + lane; i <= high; i += 32) ort[i] = H[IX(i, m - 1, ld)];

@@ -535,8 +535,9 @@ static __device__ __noinline__ int leader_ritz_basis(double* Mx, int p, int kreq
   __syncthreads();
   if (!s_ok) return -1;
   const int nz = hqr_z_warps(p, (int)(blockDim.x >> 5));
+  blk_orthes(Mx, p, p, Z, p, ort);  // whole CTA: Hessenberg form + accumulated transformation
   if ((int)threadIdx.x < 32 * (1 + nz)) {  // warp 0: QR iteration, warps 1 .. nz: Schur-vector updates
-    bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort, hp, nz);
+    bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort, hp, nz, true);
     if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
   }
   __syncthreads();
@@ -1102,9 +1103,12 @@ __device__ StepScalars inner_solve(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync&
   int applies = 0;
   // s = U^-1 L^-1 rhat[perm] at u^2, stored in u
   t.sync();
+  mark(ts.log, 36);
   op_apply<MV>(t, K.sys, (const TW*)nullptr, K.rhat, K.s, K.ybuf, ts, smem_ops);
+  mark(ts.log, 37);
   const double snorm = team_nrm2<TW>(t, K.s, n, red);
   team_zero(t, K.x, n);
+  mark(ts.log, 38);
   int keff = K.recycling ? *K.keff_io : 0;
   if (snorm == 0.0) {
     out.status = KS_CONVERGED;

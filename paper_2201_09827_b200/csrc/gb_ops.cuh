@@ -1187,9 +1187,9 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
       double* ysol = yb + s.lda;  // ybuf holds 2 ldv doubles
       if (v != nullptr) {
         if (s.a_normal)
-          seg::gemv_perm<TA, TV, true>(t, n, s.A, s.lda, s.perm, v, yb, smem, s.gemv_ns);
+          seg::gemv_perm<TA, TV, true>(t, n, s.A, s.lda, s.perm, v, yb, smem, s.gemv_ns, ts.log);
         else
-          seg::gemv_perm<TA, TV, false>(t, n, s.A, s.lda, s.perm, v, yb, smem, s.gemv_ns);
+          seg::gemv_perm<TA, TV, false>(t, n, s.A, s.lda, s.perm, v, yb, smem, s.gemv_ns, ts.log);
       } else {
         int lo, hi;
         t.rows(n, lo, hi);

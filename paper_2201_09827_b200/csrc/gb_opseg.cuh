@@ -1123,7 +1123,7 @@ __device__ __noinline__ void gemv_ldg(Team& t, int n, const TA* __restrict__ A, 
 template <class TA, class TV, bool kNormal, class Team>
 __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A, size_t lda,
                                        const int* __restrict__ perm, const TV* __restrict__ v, double* out,
-                                       void* smem_raw, int NS) {
+                                       void* smem_raw, int NS, const PhaseLog lg = PhaseLog{nullptr, 0, nullptr}) {
   constexpr int EPC = GCH / sizeof(TA);  // elements per chunk
   double* vs = reinterpret_cast<double*>(smem_raw);
   unsigned char* ring = reinterpret_cast<unsigned char*>(smem_raw) + gemv_vbytes(n);
@@ -1144,6 +1144,7 @@ __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A,
   for (int j = n + threadIdx.x; j < (int)(gemv_vbytes(n) / 8); j += NT) vs[j] = 0.0;
   for (int i = threadIdx.x; i < nrows; i += NT) rows[i] = perm[r + i * G];
   __syncthreads();
+  mark(lg, 14);
   // producer state (thread 0): next chunk to issue as (row, chunk-in-row)
   int pr = 0, pc = 0, pn = 0;
   auto issue_next = [&]() {
@@ -1204,9 +1205,11 @@ __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A,
       acc0 = acc1 = 0.0;
       ci = 0;
       ++ri;
+      mark(lg, 15);
     }
   }
   __syncthreads();
+  mark(lg, 16);
 }
 
 }  // namespace seg

@@ -76,6 +76,7 @@ struct Prob {
   double* r;
   double* xref;
   int* has_xref;
+  int inner_only;  // gb_debug_inner_solve: the inner solver alone on fl_u(rtmp), d -> dtmp
   double normA, normB;
   int ur, method;
   unsigned long long* ctr;    // [2]
@@ -209,7 +210,7 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
   gb_step_info info;
   memset(&info, 0, sizeof(info));
   t.sync();
-  const double nu = team_amax<double>(t, P.r, n, red);
+  const double nu = P.inner_only ? 1.0 : team_amax<double>(t, P.r, n, red);
   info.nu = nu;
   if (nu == 0.0 || !isfinite(nu)) {
     info.status = (nu == 0.0) ? RS_NU_ZERO : RS_NU_NONFINITE;
@@ -217,8 +218,14 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
     if (t.leader() && threadIdx.x == 0) *P.out = info;
     return;
   }
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) K.rhat[i] = (TW)F::rnd(P.r[i] / nu);
+  if (P.inner_only) {
+    // gmres_solve / gcrodr_solve on a caller's right-hand side (gmres.py:235, gcrodr.py:221)
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) K.rhat[i] = (TW)P.rtmp[i];
+  } else {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) K.rhat[i] = (TW)F::rnd(P.r[i] / nu);
+  }
   StepScalars st{0, KS_CONVERGED, 0, 0};
+  mark(ts.log, 31);
   if (P.method == METH_SIR) {
     t.sync();
     op_apply<UM>(t, K.sys, (const TW*)nullptr, (const TW*)K.rhat, K.x,
@@ -229,6 +236,7 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
     st = inner_solve(t, K, ts, sm, ops);
   }
   int its = 0;
+  mark(ts.log, 33);
   if (P.method == METH_SIR) {
     its = 1;
   } else {
@@ -236,10 +244,26 @@ __device__ void step_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops) {
     t.sync();
     for (int c = 0; c < st.ncycles; ++c) its += __ldcg(K.cycle_iters + c);
   }
+  if (P.inner_only) {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) P.dtmp[i] = (double)K.x[i];
+    info.ferr = info.nbe = info.cbe = NAN;
+    info.inner_iters = its;
+    info.ncycles = st.ncycles;
+    info.status = st.status;
+    info.applies = st.applies;
+    info.keff = st.keff;
+    if (t.leader() && threadIdx.x == 0) {
+      *P.out = info;
+      *P.epoch = ts.epoch;
+    }
+    return;
+  }
   for (int i = lo + threadIdx.x; i < hi; i += blockDim.x)
     P.xs[i] = fl_add<TW>(P.xs[i], F::scale(nu, K.x[i]));
   t.sync();
+  mark(ts.log, 34);
   info.ferr = P.has_xref[0] ? forward_error(t, (const TW*)P.xs, P.xref, n, red) : NAN;
+  mark(ts.log, 35);
   ResidOut ro = residual_check(t, K.sys.A, K.sys.lda, n, (const TW*)P.xs, P.b, P.r, P.ur, P.normA, P.normB, red);
   info.nbe = ro.nbe;
   info.cbe = ro.cbe;
@@ -309,11 +333,18 @@ __device__ void debug_body(Team& t, Prob<TW, TF, MV>& P, double* sm, void* ops, 
     op_apply<M>(t, K.sys, (const TW*)K.rhat, (const TW*)nullptr, K.w, yb, ts, ops);
   } else if (what == 1 || what == 3) {
     op_apply<M>(t, K.sys, (const TW*)nullptr, (const TW*)K.rhat, K.w, yb, ts, ops);
+  } else if (what == 5) {
+    // check_convergence's residual and backward errors (refine.py:194-208)
+    ResidOut ro = residual_check(t, K.sys.A, K.sys.lda, n, (const TW*)K.rhat, P.b, P.dtmp, P.ur, P.normA, P.normB, red);
+    if (t.leader() && threadIdx.x == 0) {
+      P.out->nbe = ro.nbe;
+      P.out->cbe = ro.cbe;
+    }
   } else {
     residual_check(t, K.sys.A, K.sys.lda, n, (const TW*)K.rhat, P.b, P.dtmp, P.ur, 1.0, 1.0, red);
   }
   t.sync();
-  if (what != 2)
+  if (what != 2 && what != 5)
     for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) P.dtmp[i] = (double)K.w[i];
   if (t.leader() && threadIdx.x == 0) *P.epoch = ts.epoch;
 }
@@ -793,6 +824,7 @@ struct gb_solver {
   // (gb_opseg.cuh sweep_bsp), GEMV bulk-copy stages, A entries all normal
   double *bigl = nullptr, *bigu = nullptr;
   int nbig = 0, gemv_ns = 0, a_normal = 0;
+  int inner_only = 0;      // next step launch runs the inner solver alone (gb_debug_inner_solve)
   int max_cycles_cap = 0;  // o.max_cycles at creation (workspace size); o.max_cycles may be lowered
   PivKey* lu_ckey = nullptr;
   double *lu_crow = nullptr, *lu_rowk = nullptr;
@@ -812,6 +844,7 @@ struct gb_solver {
   uint4* ytag = nullptr;
   unsigned long long* plog = nullptr;  // phase log (diagnostics), 1 + 2 * cap
   int plog_cap = 0;
+  bool plog_host = false;  // GB_PLOG_HOST=1: mapped pinned host memory (readable after a fault)
   GridCtl* ctl = nullptr;
   double* partials = nullptr;
   int kmax = 0;
@@ -916,6 +949,7 @@ struct Impl {
     P.r = s->r;
     P.xref = s->xref;
     P.has_xref = s->has_xref;
+    P.inner_only = s->inner_only;
     P.normA = s->normA;
     P.normB = s->normB;
     P.ur = s->o.ur == GB_QUAD ? UR_DD : (s->o.ur == GB_DOUBLE ? UR_F64 : UR_F32);
@@ -945,7 +979,7 @@ struct Impl {
     P.xuinvl = s->xuinvl;
     P.rtmp = s->rtmp;
     P.dtmp = s->dtmp;
-    P.log = PhaseLog{s->plog, s->plog_cap};
+    P.log = PhaseLog{s->plog, s->plog_cap, s->plog_host ? s->plog + 1 + 2 * (size_t)s->plog_cap : nullptr};
     return P;
   }
 
@@ -1456,7 +1490,7 @@ struct Impl {
     auto go = [&](auto kc, auto kcl, auto kg) {
       return s->G == 1 ? launch(s, kc, P, what) : s->cluster ? launch(s, kcl, P, what) : launch(s, kg, P, what);
     };
-    if (what == 2) {
+    if (what == 2 || what == 5) {
       // residual(a, x, b, ctx): the mode template is irrelevant for it
       P.ur = fmt == GB_QUAD ? UR_DD : (fmt == GB_DOUBLE ? UR_F64 : UR_F32);
       e = go(k_debug<MV, TW, TF, MV, CtaTeam>, k_debug<MV, TW, TF, MV, ClusterTeam>, k_debug<MV, TW, TF, MV, GridTeam>);

@@ -210,16 +210,16 @@ inline EncodeTiledFn encode_fn() {
 // 2-D fp16 map over a row-major matrix (rows x cols, row pitch in elements),
 // box = box_rows x 32 columns, SWIZZLE_64B (the UMMA K-major SW64 atom)
 inline bool make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
-                     uint32_t box_rows) {
+                     uint32_t box_rows, uint32_t box_cols = BK, bool swizzle128 = false) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return false;
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {pitch_elems * 2};
-  const cuuint32_t box[2] = {BK, box_rows};
+  const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // W[r0:r0+M, c0:c0+N] -= W[r0:r0+M, k0:k0+K] * W[k0:k0+K, c0:c0+N]  (fp32
@@ -261,12 +261,24 @@ inline cudaError_t tc_update(__half* W, size_t ld, int nrows, int r0, int c0, in
 namespace tcg2 {
 
 constexpr int BM = 128, PM = 256, BN = 256, HN = 128, BK = 32;
-constexpr int STAGES = 12;
 constexpr int A_BYTES = BM * BK * 2;            // 8 KB
 constexpr int B_BYTES = HN * BK * 2;            // 8 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 16 KB per CTA
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
-constexpr int NTHREADS = 384;  // TMA, MMA, TMEM, (idle), 8 epilogue warps
+// kTmaC: the CTA's 128 x 256 tile of C is staged in shared memory (four
+// 128 x 64 boxes, SWIZZLE_128B) by TMA under the tile's MMAs, updated in
+// place by the epilogue warps and written back by TMA stores -- all global
+// traffic of the epilogue is bulk and coalesced (row-per-lane global accesses
+// cost 32 LSU wavefronts per instruction).  Needs M, N multiples of 256 (a
+// TMA store cannot mask the rows / columns of a partial tile).
+constexpr int C_BOX_COLS = 64;
+constexpr int C_BOX_BYTES = BM * C_BOX_COLS * 2;  // 16 KB
+constexpr int C_BYTES = 4 * C_BOX_BYTES;          // 64 KB
+template <bool kTmaC>
+struct Cfg {
+  static constexpr int STAGES = kTmaC ? 8 : 12;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + (kTmaC ? C_BYTES : 0) + 1024 + 512;
+};
+constexpr int NTHREADS = 384;  // TMA, MMA, TMEM, C loader, 8 epilogue warps
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -319,17 +331,30 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(tc::smem_u32(src))
+               : "memory");
+}
+
+template <bool kTmaC>
 static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    k_tc_update2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, __half* W,
-                 size_t ld, int r0, int c0, int M, int N, int k0, int K) {
+    k_tc_update2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_c, __half* W, size_t ld, int r0, int c0, int M, int N, int k0,
+                 int K) {
+  constexpr int STAGES = Cfg<kTmaC>::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // the same offset in both CTAs (the dynamic window starts at the same address)
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  unsigned char* csm = smem + STAGES * STAGE_BYTES;  // C tile (kTmaC), 1024-byte aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(csm + (kTmaC ? C_BYTES : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = tempty + 2;      // C tile landed
+  uint64_t* cfree = cfull + 1;       // C tile written back, buffer reusable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -345,9 +370,12 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       tc::mbar_init(tfull + i, 1);
       tc::mbar_init(tempty + i, 16);  // one elected arrive per epilogue warp of the pair
     }
+    tc::mbar_init(cfull, 1);
+    tc::mbar_init(cfree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tcg::prefetch_map(&map_a);
     tcg::prefetch_map(&map_b);
+    if (kTmaC) tcg::prefetch_map(&map_c);
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
   tc::fence_before();
@@ -396,6 +424,71 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       }
       commit_pair(tfull + acc);
     }
+  } else if (kTmaC && warp == 3 && lane == 0) {
+    // ---- C loader (both CTAs): this CTA's 128 x 256 tile of C, as soon as the
+    // previous tile has been written back
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      const int ti = t / tn, tj = t % tn;
+      if (it > 0) tc::mbar_wait(cfree, (uint32_t)((it - 1) & 1));
+      tcg::mbar_expect_tx(cfull, C_BYTES);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        tcg::tma_2d(csm + b * C_BOX_BYTES, &map_c, c0 + tj * BN + b * C_BOX_COLS, r0 + ti * PM + (int)rank * BM, cfull);
+    }
+  } else if (kTmaC && warp >= 4) {
+    // ---- epilogue, C through shared memory: thread = (row 32 q + lane, column
+    // half hc); element (row, 16-byte chunk c) of a box sits at
+    // row * 128 + ((c ^ (row & 7)) << 4) (SWIZZLE_128B)
+    const int q = warp & 3, hc = (warp - 4) >> 2;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
+      const int ti = t / tn, tj = t % tn;
+      const int acc = it & 1;
+      tc::mbar_wait(cfull, (uint32_t)(it & 1));
+      tc::mbar_wait(tfull + acc, (uint32_t)((it >> 1) & 1));
+      tc::fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + hc * 128);
+      auto upd = [](unsigned c, float a, float b) -> unsigned {
+        __half2 h = *reinterpret_cast<__half2*>(&c);
+        const float2 f = __half22float2(h);
+        h = __floats2half2_rn(f.x - a, f.y - b);
+        return *reinterpret_cast<unsigned*>(&h);
+      };
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        float v[32];
+        tc::tmem_ld32(tbase + (uint32_t)(ch * 32), v);
+        unsigned char* box = csm + (hc * 2 + (ch >> 1)) * C_BOX_BYTES + row * 128;
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          const int c = (ch & 1) * 4 + z;
+          uint4* p = reinterpret_cast<uint4*>(box + ((c ^ (row & 7)) << 4));
+          const uint4 cc = *p;
+          uint4 o;
+          o.x = upd(cc.x, v[8 * z + 0], v[8 * z + 1]);
+          o.y = upd(cc.y, v[8 * z + 2], v[8 * z + 3]);
+          o.z = upd(cc.z, v[8 * z + 4], v[8 * z + 5]);
+          o.w = upd(cc.w, v[8 * z + 6], v[8 * z + 7]);
+          *p = o;
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_addr(tempty + acc));  // accumulator drained
+      tc::fence_proxy_async();                                       // smem writes -> async proxy
+      asm volatile("bar.sync 2, 256;" ::: "memory");                 // the 8 epilogue warps
+      if (warp == 4 && lane == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          tma_store_2d(&map_c, c0 + tj * BN + b * C_BOX_COLS, r0 + ti * PM + (int)rank * BM, csm + b * C_BOX_BYTES);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        tcg::mbar_arrive(cfree);
+      }
+    }
+    if (warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   } else if (warp >= 4) {
     // ---- epilogue (both CTAs, 8 warps): warp 4 + q + 4 h owns TMEM lanes
     // 32 q .. 32 q + 31 (rows 128 rank + 32 q + lane of the pair tile) and the
@@ -458,14 +551,15 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 }
 
 // pairs that can be co-resident (148 SMs = 74 TPCs unless a GPC is short)
-inline int max_pairs() {
+template <bool kTmaC>
+inline int max_pairs_t() {
   static int pairs = -1;
   if (pairs < 0) {
-    cudaFuncSetAttribute(k_tc_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(k_tc_update2<kTmaC>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<kTmaC>::SMEM_BYTES);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74);
     cfg.blockDim = dim3(NTHREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = Cfg<kTmaC>::SMEM_BYTES;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -474,7 +568,7 @@ inline int max_pairs() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (const void*)k_tc_update2, &cfg) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)k_tc_update2<kTmaC>, &cfg) != cudaSuccess || n < 1) {
       cudaGetLastError();
       n = 64;
     }
@@ -482,19 +576,29 @@ inline int max_pairs() {
   }
   return pairs;
 }
+inline int max_pairs() { return max_pairs_t<true>(); }
 
-// same contract as tcg::tc_update
+// same contract as tcg::tc_update; tma_c = -1 picks the shared-memory C path
+// whenever the update is made of whole 256 x 256 tiles
 inline cudaError_t tc_update(__half* W, size_t ld, int nrows, int r0, int c0, int M, int N, int k0, int K,
-                             __half* Bt, cudaStream_t st) {
+                             __half* Bt, cudaStream_t st, int tma_c = -1) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   dim3 tb(32, 8), tg((N + 31) / 32, (K + 31) / 32);
   tcg::k_transpose_u12<<<tg, tb, 0, st>>>(W, ld, k0, c0, K, N, Bt);
-  CUtensorMap ma, mb;
-  if (!tcg::make_map(&ma, W, (uint64_t)nrows, ld, ld, BM) || !tcg::make_map(&mb, Bt, (uint64_t)N, (uint64_t)K, K, HN))
+  const bool whole = M % PM == 0 && N % BN == 0 && c0 % 8 == 0;
+  const bool use_c = tma_c < 0 ? whole : (tma_c != 0 && whole);
+  CUtensorMap ma, mb, mc;
+  if (!tcg::make_map(&ma, W, (uint64_t)nrows, ld, ld, BM) || !tcg::make_map(&mb, Bt, (uint64_t)N, (uint64_t)K, K, HN) ||
+      !tcg::make_map(&mc, W, (uint64_t)nrows, ld, ld, BM, C_BOX_COLS, true))
     return cudaErrorInvalidValue;
   const int ntiles = ((M + PM - 1) / PM) * ((N + BN - 1) / BN);
-  const int pairs = std::min(ntiles, max_pairs());
-  k_tc_update2<<<2 * pairs, NTHREADS, SMEM_BYTES, st>>>(ma, mb, W, ld, r0, c0, M, N, k0, K);
+  if (use_c) {
+    const int pairs = std::min(ntiles, max_pairs_t<true>());
+    k_tc_update2<true><<<2 * pairs, NTHREADS, Cfg<true>::SMEM_BYTES, st>>>(ma, mb, mc, W, ld, r0, c0, M, N, k0, K);
+  } else {
+    const int pairs = std::min(ntiles, max_pairs_t<false>());
+    k_tc_update2<false><<<2 * pairs, NTHREADS, Cfg<false>::SMEM_BYTES, st>>>(ma, mb, mc, W, ld, r0, c0, M, N, k0, K);
+  }
   return cudaGetLastError();
 }
 

@@ -343,6 +343,32 @@ def _refine(a, b, cfg: RefineConfig, *, trace: list | None = None, grid_ctas: in
             solver.close()
 
 
+def check_convergence(a, b, x, d, history, precisions: PrecisionTriple, c_conv: float = 2.0,
+                      inner_stagnated: bool = False, norm_a_inf: float | None = None,
+                      norm_b_inf: float | None = None, ferr: float = float("nan")) -> ConvergenceDecision:
+    """refine.py:172-229: residual at u_r, nbe, cbe on the device
+    (gb_backward_errors), the decision rules on the host (``classify``).  The
+    norms are those of fl_u(a), fl_u(b) as the loop holds them; passing other
+    values is not supported on the device path."""
+    del d  # unused by the reference too
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    n = a.shape[0]
+    if a.shape != (n, n) or b.shape != (n,) or x.shape != (n,):
+        raise ValueError("dimension mismatch in check_convergence")
+    if norm_a_inf is not None or norm_b_inf is not None:
+        raise NotImplementedError("the device computes ||A||_inf and ||b||_inf itself")
+    cfg = RefineConfig(precisions, Method.GMRES_IR, m=min(n, 2))
+    solver = _lib.Solver(n, make_options(cfg, n))
+    try:
+        solver.set_system(a, b)
+        _, nbe, cbe = solver.backward_errors(x)
+    finally:
+        solver.close()
+    return classify(nbe, cbe, ferr, list(history), precisions, c_conv, inner_stagnated)
+
+
 def sir(a, b, cfg: RefineConfig) -> RefinementReport:
     if cfg.method is not Method.SIR:
         raise ValueError("sir() requires cfg.method == Method.SIR")

@@ -222,3 +222,53 @@ def test_grid_team_solve(gpu):
     assert all(abs(x - y) <= 1 for x, y in zip(rep.inner_iters, ref.inner_iters)), (rep.inner_iters, ref.inner_iters)
     for got, want in ((rep.nbe_history[-1], ref.nbe_history[-1]), (rep.ferr_history[-1], ref.ferr_history[-1])):
         assert got <= 10 * want + 2 * 2.0 ** -53, (got, want)
+
+
+def test_inner_solver_mirrors(gpu):
+    """gmres_solve / gcrodr_solve (gb_debug_inner_solve) and check_convergence
+    (gb_backward_errors) against the oracle's restatement of gmres.py:235-311,
+    gcrodr.py:221-419 and refine.py:172-229 on the config-1 system: cold GMRES,
+    cold GCRO-DR, then a warm-started GCRO-DR on a second right-hand side."""
+    import paper_2201_09827_b200 as gb
+    from paper_2201_09827_b200 import densela, problems
+
+    a, b = problems.config_problem(problems.CONFIGS["cfg1"])
+    a_u, b_u = O.rnd(a, "single"), O.rnd(b, "single")
+    n = a.shape[0]
+    f = densela.lu_factor(a_u, Format.HALF)
+    of = O.lu_factor(a_u, "half")
+    rng = np.random.default_rng(5)
+    r1 = O.rnd(rng.standard_normal(n), "single")
+    r2 = O.rnd(rng.standard_normal(n), "single")
+    try:
+        g = gb.gmres_solve(a_u, f, r1, gb.GmresConfig(m=40, tau=1e-4, matvec_ctx=Format.DOUBLE, work_fmt=Format.SINGLE))
+        og = O.gmres(a_u, of, r1, 40, 1e-4, "double", "single")
+        assert g.converged == og.converged and len(g.iterations_per_cycle) == len(og.cycles)
+        assert abs(g.total_iterations - og.total) <= 1, (g.iterations_per_cycle, og.cycles)
+        assert np.max(np.abs(g.solution - og.solution)) <= 2e-3 * np.max(np.abs(og.solution))
+        cfg = gb.GcrodrConfig(m=40, k=5, tau=1e-4, matvec_ctx=Format.DOUBLE, work_fmt=Format.SINGLE,
+                              collect_diagnostics=True)
+        c1, space = gb.gcrodr_solve(a_u, f, r1, cfg)
+        o1, orec = O.gcrodr(a_u, of, r1, 40, 5, 1e-4, "double", "single")
+        assert c1.converged == o1.converged and abs(c1.total_iterations - o1.total) <= 1, (c1, o1.cycles)
+        assert space is not None and space.k_eff == orec.k_eff
+        c2, space2 = gb.gcrodr_solve(a_u, f, r2, cfg, recycle_in=space)
+        o2, _ = O.gcrodr(a_u, of, r2, 40, 5, 1e-4, "double", "single", recycle_in=orec)
+        assert c2.converged == o2.converged and abs(c2.total_iterations - o2.total) <= 1, (c2, o2.cycles)
+        assert c2.operator_applies == o2.applies  # warm-start applications are counted as operator work
+        assert np.max(np.abs(c2.solution - o2.solution)) <= 2e-3 * np.max(np.abs(o2.solution))
+        with pytest.raises(ValueError):
+            gb.gcrodr_solve(a_u, f, r1, gb.GcrodrConfig(m=5, k=5, tau=1e-4, matvec_ctx=Format.DOUBLE,
+                                                        work_fmt=Format.SINGLE))
+    finally:
+        f.close()
+    # check_convergence: one step's decision from a perturbed solution
+    x = O.rnd(np.linalg.solve(a_u, b_u) * (1 + 1e-5), "single")
+    prec = PrecisionTriple(Format.HALF, Format.SINGLE, Format.DOUBLE)
+    d = gb.check_convergence(a, b, x, None, [], prec)
+    state, reason, nbe, cbe = O.check_convergence(a_u, b_u, x, [], "single", 2.0, False, O.inf_norm(a_u),
+                                                  O.inf_norm(b_u), float("nan"), "double")
+    assert d.state == state and (d.reason.value if d.reason else None) == reason
+    assert abs(d.nbe - nbe) <= 1e-6 * nbe and abs(d.cbe - cbe) <= 1e-6 * cbe  # fp64 residual, different summation order
+    d2 = gb.check_convergence(a, b, x, None, [], prec, inner_stagnated=True)
+    assert d2.state == "diverged" and d2.reason is gb.DivergenceReason.INNER_STAGNATION

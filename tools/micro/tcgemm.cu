@@ -10,7 +10,7 @@ using namespace gb;
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 8192;
   const int K = argc > 2 ? atoi(argv[2]) : 256;
-  const int pairmode = argc > 3 ? atoi(argv[3]) : 1;  // 1: CTA-pair kernel (cta_group::2), 0: one-CTA kernel
+  const int pairmode = argc > 3 ? atoi(argv[3]) : 1;  // 1: CTA-pair kernel (cta_group::2, C through smem + TMA when whole tiles), 2: pair kernel, register epilogue, 0: one-CTA kernel
   const size_t ld = (n + 31) & ~31;
   std::mt19937 rng(3);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
@@ -23,7 +23,7 @@ int main(int argc, char** argv) {
   const int k0 = 0, r0 = K, c0 = K, M = n - K, N = n - K;
   int nsm = 148;
   auto upd = [&]() {
-    return pairmode ? tcg2::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, 0)
+    return pairmode ? tcg2::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, 0, pairmode == 2 ? 0 : -1)
                     : tcg::tc_update(dW, ld, n, r0, c0, M, N, k0, K, dBt, nsm, 0);
   };
   if (pairmode) printf("co-resident CTA pairs: %d\n", tcg2::max_pairs());
