@@ -192,8 +192,12 @@ def _inputs(spec, rank: int = 0, world: int = 1):
             except Exception:
                 pass
         t0 = time.perf_counter()
-        a, b = problems.config_problem(spec, 0)
-        _log(f"generated {spec.name} inputs (n={spec.n}) in {time.perf_counter() - t0:.1f}s")
+        a, b = _device_randsvd(spec) if spec.kind == "randsvd" and spec.n >= 8192 else (None, None)
+        how = "device QR"
+        if a is None:
+            a, b = problems.config_problem(spec, 0)
+            how = "host LAPACK"
+        _log(f"generated {spec.name} inputs (n={spec.n}, {how}) in {time.perf_counter() - t0:.1f}s")
         if spec.n >= 2048:
             try:
                 np.savez(cache + ".tmp.npz", a=a, b=b)
@@ -207,6 +211,44 @@ def _inputs(spec, rank: int = 0, world: int = 1):
     for i, sysid in enumerate(idx):
         A[i], B[i] = problems.config_problem(spec, sysid)
     return A, B
+
+
+def _device_randsvd(spec):
+    """The reference's randsvd construction (matgen.py:70-92: Philox(seed)
+    Gaussians, two Haar factors from sign-fixed QR, geometric singular values,
+    A = (P * sigma) Q^T) with the two n x n QR factorisations and the product
+    on the GPU -- minutes of host LAPACK become seconds.  Same seeded Gaussian
+    stream and the same distribution as the reference's generator, not the
+    same bits (cuSOLVER's Householder QR rounds differently from LAPACK's);
+    no reference run exists at these sizes to be bit-compatible with (SURVEY
+    F8).  Returns (None, None) without a GPU."""
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return None, None
+    except Exception:
+        return None, None
+    from paper_2201_09827_b200 import problems
+
+    n = spec.n
+    rng = np.random.Generator(np.random.Philox(1))
+    sig = torch.from_numpy(spec.param ** (-np.arange(n) / (n - 1))).cuda()
+
+    def haar():
+        g = torch.from_numpy(rng.standard_normal((n, n))).cuda()
+        q, r = torch.linalg.qr(g)
+        d = torch.sign(torch.diagonal(r)).clone()
+        d[d == 0] = 1.0
+        del g, r
+        return q * d[None, :]
+
+    left = haar()
+    right = haar()
+    a = ((left * sig[None, :]) @ right.T).cpu().numpy()
+    del left, right
+    torch.cuda.empty_cache()
+    return a, problems.rhs_normal(n, 1)
 
 
 def _alg_bytes(spec, trace) -> float:

@@ -379,7 +379,18 @@ static __device__ __noinline__ double blk_cond2(double* b, int ld, int p, double
         for (int r = i + 1; r < p; ++r) wv = __fma_rn(b[IX(r, i, ld)], b[IX(r, l, ld)], wv);
         wv *= tj;
         b[IX(i, l, ld)] -= wv;
-        for (int r = i + 1; r < p; ++r) b[IX(r, l, ld)] = __fma_rn(-wv, b[IX(r, i, ld)], b[IX(r, l, ld)]);
+        // loads in batches ahead of the stores (the matrix may live in global memory)
+        for (int r0 = i + 1; r0 < p; r0 += 8) {
+          double x[8], y[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            x[u] = r0 + u < p ? b[IX(r0 + u, i, ld)] : 0.0;
+            y[u] = r0 + u < p ? b[IX(r0 + u, l, ld)] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (r0 + u < p) b[IX(r0 + u, l, ld)] = __fma_rn(-wv, x[u], y[u]);
+        }
       }
     }
     __syncthreads();
@@ -414,7 +425,17 @@ static __device__ __noinline__ double blk_cond2(double* b, int ld, int p, double
         for (int c = i + 2; c < p; ++c) wv = __fma_rn(b[IX(i, c, ld)], b[IX(r, c, ld)], wv);
         wv *= tj;
         b[IX(r, i + 1, ld)] -= wv;
-        for (int c = i + 2; c < p; ++c) b[IX(r, c, ld)] = __fma_rn(-wv, b[IX(i, c, ld)], b[IX(r, c, ld)]);
+        for (int c0 = i + 2; c0 < p; c0 += 8) {
+          double x[8], y[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            x[u] = c0 + u < p ? b[IX(i, c0 + u, ld)] : 0.0;
+            y[u] = c0 + u < p ? b[IX(r, c0 + u, ld)] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c0 + u < p) b[IX(r, c0 + u, ld)] = __fma_rn(-wv, x[u], y[u]);
+        }
       }
     }
     __syncthreads();

@@ -361,7 +361,63 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
     // next basis column is loaded before each reduction (the loads do not
     // depend on it), so one team reduction is the only latency per i.
     double hprev = 0.0;
-    {
+    // Large cooperative grids run the sweep on a sub-team of T CTAs (1024 rows
+    // each): every link is one exchange through global memory, and T = 16
+    // slots are polled in a fraction of the time 148 take.  The other CTAs
+    // wait at the barrier below; the h column is broadcast through colbuf.
+    bool sub_done = false;
+    if constexpr (Team::kGrid) {
+      int T = 0;
+      if (!t.clu && t.spart == nullptr && t.size() > 32 && j + 2 <= kColBuf) T = min(32, (n + 1023) / 1024);
+      if (T > 0) {
+      sub_done = true;
+      constexpr int QW = 4;
+      if (t.rank() < T) {
+        const int per = (((n + T - 1) / T) + 31) & ~31;  // <= 1024 rows
+        const int slo = min(n, t.rank() * per), shi = min(n, slo + per);
+        TW wr[QW], vc[QW], vn[QW];
+#pragma unroll
+        for (int q = 0; q < QW; ++q) {
+          const int r = slo + threadIdx.x + q * blockDim.x;
+          wr[q] = r < shi ? __ldcg(K.w + r) : TW(0);
+          vc[q] = r < shi ? K.V[r] : TW(0);
+        }
+        for (int i = 0; i <= j; ++i) {
+          typename F::Acc a = typename F::Acc(0);
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const int r = slo + threadIdx.x + q * blockDim.x;
+            if (r < shi) {
+              if (i > 0) wr[q] = F::axpy(-hprev, vn[q], wr[q]);
+              a = F::mac(a, vc[q], wr[q]);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const int r = slo + threadIdx.x + q * blockDim.x;
+            vn[q] = vc[q];
+            vc[q] = (r < shi && i < j) ? K.V[(size_t)(i + 1) * ldv + r] : TW(0);
+          }
+          a = t.template reduce1_sub<typename F::Acc>(a, reinterpret_cast<typename F::Acc*>(red), T);
+          hprev = (double)a;
+          if (threadIdx.x == 0) col[i] = hprev;
+        }
+#pragma unroll
+        for (int q = 0; q < QW; ++q) {
+          const int r = slo + threadIdx.x + q * blockDim.x;
+          if (r < shi) K.w[r] = F::axpy(-hprev, vn[q], wr[q]);
+        }
+        __syncthreads();
+        if (t.leader())
+          for (int i = threadIdx.x; i <= j; i += blockDim.x) t.colbuf()[i] = col[i];
+      }
+      t.sync();
+      for (int i = threadIdx.x; i <= j; i += blockDim.x) col[i] = __ldcg(t.colbuf() + i);
+      hprev = __ldcg(t.colbuf() + j);
+      __syncthreads();
+      }
+    }
+    if (!sub_done) {
       constexpr int QW = 4;  // rows per thread: a CTA slice has <= 4 * blockDim rows
       TW wr[QW], vc[QW], vn[QW];
 #pragma unroll

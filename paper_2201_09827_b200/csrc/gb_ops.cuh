@@ -175,6 +175,7 @@ struct SysView {
   int nbig = 0;
   int gemv_ns = 0;
   int a_normal = 0;
+  int sweep_la = 0;  // look-ahead form of the big-block sweeps (seg::sweep_la)
 };
 
 // progress counters of the flag-based TRSV (one per direction)
@@ -1197,9 +1198,15 @@ __device__ void op_apply(Team& t, const SysView<TA, TF>& s, const TV* v, const T
       }
       t.sync();
       mark(ts.log, 11);
-      seg::sweep_bsp<TF, true>(t, n, s.nbig, s.LU, s.ldf, s.bigl, yb, ysol, seg::OutNone{}, smem);
-      mark(ts.log, 12);
-      seg::sweep_bsp<TF, false>(t, n, s.nbig, s.LU, s.ldf, s.bigu, ysol, yb, seg::OutTo<TW>{w}, smem);
+      if (s.sweep_la) {
+        seg::sweep_la<TF, true>(t, n, s.nbig, s.LU, s.ldf, s.bigl, yb, ysol, seg::OutNone{}, smem);
+        mark(ts.log, 12);
+        seg::sweep_la<TF, false>(t, n, s.nbig, s.LU, s.ldf, s.bigu, ysol, yb, seg::OutTo<TW>{w}, smem);
+      } else {
+        seg::sweep_bsp<TF, true>(t, n, s.nbig, s.LU, s.ldf, s.bigl, yb, ysol, seg::OutNone{}, smem);
+        mark(ts.log, 12);
+        seg::sweep_bsp<TF, false>(t, n, s.nbig, s.LU, s.ldf, s.bigu, ysol, yb, seg::OutTo<TW>{w}, smem);
+      }
       mark(ts.log, 13);
       ts.epoch++;
       return;

@@ -1157,8 +1157,10 @@ __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A,
     ++pn;
     if (++pc == cpr) pc = 0, ++pr;
   };
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    fence_async_smem();  // earlier generic-proxy accesses of the ring before the async writes
     while (pn < min(NS, total)) issue_next();
+  }
   double acc0 = 0.0, acc1 = 0.0;
   int ri = 0, ci = 0, st = 0;
   unsigned ph = 0;
@@ -1208,6 +1210,15 @@ __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A,
       mark(lg, 15);
     }
   }
+  __syncthreads();
+  // the ring's barriers are re-initialised by the next call (the region is
+  // shared with the sweeps' staging and the leader's scratch in between):
+  // invalidate them first -- re-initialising a live mbarrier is undefined,
+  // and a stage that has completed an odd number of phases did fault the
+  // next call's first wait at n = 16384 (111 rows x 4 chunks on 5 stages)
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NS; ++i)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + i)) : "memory");
   __syncthreads();
   mark(lg, 16);
 }

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -823,7 +824,7 @@ struct gb_solver {
   // grid teams with an fp64 operator: inverses of the big diagonal blocks
   // (gb_opseg.cuh sweep_bsp), GEMV bulk-copy stages, A entries all normal
   double *bigl = nullptr, *bigu = nullptr;
-  int nbig = 0, gemv_ns = 0, a_normal = 0;
+  int nbig = 0, gemv_ns = 0, a_normal = 0, sweep_la = 0;
   int inner_only = 0;      // next step launch runs the inner solver alone (gb_debug_inner_solve)
   int max_cycles_cap = 0;  // o.max_cycles at creation (workspace size); o.max_cycles may be lowered
   PivKey* lu_ckey = nullptr;
@@ -910,6 +911,7 @@ struct Impl {
       K.sys.nbig = s->nbig;
       K.sys.gemv_ns = s->gemv_ns;
       K.sys.a_normal = s->a_normal;
+      K.sys.sweep_la = s->sweep_la;
     }
     K.V = (TW*)s->V;
     K.w = (TW*)s->w;
@@ -1002,7 +1004,7 @@ struct Impl {
       // bulk-copy GEMV (v as fp64 + a ring filling the rest of 227 KB) and the
       // big-block substitution's staged vector (sweep_bsp)
       const size_t base = sm_doubles(s->o.m, s->o.k) * sizeof(double);
-      b = std::max(b, base + std::max(seg::gemv_smem(s->n, s->gemv_ns), (size_t)s->nbig * 8 + 64));
+      b = std::max(b, base + std::max(seg::gemv_smem(s->n, s->gemv_ns), (size_t)s->nbig * 16 + 64));
     }
     if (s->G > 1 && !s->cluster && fast_cap(s->o.m, s->o.k) == 0) {
       // packed Hessenberg storage of the harmonic-Ritz eigenproblem (dimension <= m)
@@ -1155,7 +1157,7 @@ struct Impl {
       s->epoch = a.take<unsigned long long>(2);
       s->ytag = a.take<uint4>(2 * (size_t)ldv);
       s->norms = a.take<unsigned long long>(4);
-      s->ctl = a.take<GridCtl>(1 + (2 * kLinkSlots * 16 + sizeof(GridCtl) - 1) / sizeof(GridCtl));  // + reduce1 slots
+      s->ctl = a.take<GridCtl>(1 + (kCtlExtraBytes + sizeof(GridCtl) - 1) / sizeof(GridCtl));  // + reduce1 slots, broadcast
       s->partials = a.take<double>((size_t)2 * s->G * s->kmax);
       s->cycle_iters = a.take<int>(m * 0 + s->o.max_cycles + 4);
       s->cycle_keff = a.take<int>(s->o.max_cycles + 4);
@@ -1185,6 +1187,8 @@ struct Impl {
     a.base = (char*)s->mem;
     plan(true);
     if (s->bigl != nullptr) {
+      const char* la = std::getenv("GB_SWEEP_LA");
+      s->sweep_la = (la && la[0] == '1') ? 1 : 0;
       // 227 KB per CTA = dynamic + static: the step kernels declare 7 KB of
       // static shared memory (reduction / pivot scratch), reserve 8 KB for it
       const size_t budget = 227 * 1024 - sm_doubles(s->o.m, s->o.k) * sizeof(double) - 8192;

@@ -92,6 +92,11 @@ GB_DEVICE bool team_tget(const uint4* p, unsigned tag, double& v) {
   return y == tag && w == tag;
 }
 constexpr int kLinkSlots = 160;  // >= the largest grid team (148 CTAs)
+constexpr int kSubSlots = 32;    // sub-team of the Gram-Schmidt sweep (reduce1_sub)
+constexpr int kColBuf = 256;     // doubles broadcast from the sub-team to the grid
+// bytes that follow the GridCtl word in global memory: full-team slots (2 sets),
+// sub-team slots (2 sets), broadcast buffer
+constexpr size_t kCtlExtraBytes = 2 * kLinkSlots * 16 + 2 * kSubSlots * 16 + kColBuf * 8;
 
 // number of CTAs in this thread-block cluster (1 without a cluster launch)
 GB_DEVICE unsigned cluster_ncta() {
@@ -119,15 +124,51 @@ struct GridTeam {
   // tagged single-value reductions (reduce1, cooperative grids): links done by
   // this launch and the count carried over from earlier launches (the tags
   // must not repeat while a slot still holds an old one); slots follow *ctl
-  unsigned long long link_base = 0;
-  unsigned nlink = 0;
+  unsigned long long link_base = 0, sub_base = 0;
+  unsigned nlink = 0, nsub = 0;
 
   GB_DEVICE void links_begin() {
-    if (ctl != nullptr) link_base = *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[0]);
+    if (ctl != nullptr) {
+      link_base = *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[0]);
+      sub_base = *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[2]);
+    }
   }
   GB_DEVICE void links_end() {
-    if (ctl != nullptr && r == 0 && threadIdx.x == 0 && nlink != 0)
-      *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[0]) = link_base + nlink;
+    if (ctl != nullptr && r == 0 && threadIdx.x == 0) {
+      if (nlink != 0) *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[0]) = link_base + nlink;
+      if (nsub != 0) *reinterpret_cast<volatile unsigned long long*>(&ctl->pad[2]) = sub_base + nsub;
+    }
+  }
+  GB_DEVICE uint4* sub_slots() { return reinterpret_cast<uint4*>(ctl + 1) + 2 * kLinkSlots; }
+  GB_DEVICE double* colbuf() { return reinterpret_cast<double*>(sub_slots() + 2 * kSubSlots); }
+  // reduce1 over the first T <= 32 CTAs only (the others do not call): one
+  // tagged slot per CTA, a single poll per lane.  The Gram-Schmidt sweep of a
+  // large grid team runs on such a sub-team: its links are pure exchange
+  // latency, and polling 16 slots is faster than polling 148.
+  template <class T_>
+  __device__ T_ reduce1_sub(T_ v, T_* scratch, int T) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      T_ tsum = lane < nw ? scratch[lane] : T_(0);
+      tsum = warp_sum(tsum);
+      const unsigned tag = (unsigned)((sub_base + nsub) % 0xffffffffull) + 1u;
+      uint4* slots = sub_slots() + (size_t)(nsub & 1u) * kSubSlots;
+      if (lane == 0) team_tput(slots + r, (double)tsum, tag);
+      double x = 0.0;
+      bool ok = lane >= T;
+      do {
+        if (!ok) ok = team_tget(slots + lane, tag, x);
+      } while (!__all_sync(0xffffffffu, ok));
+      T_ acc = lane < T ? (T_)x : T_(0);
+      acc = warp_sum(acc);
+      if (lane == 0) scratch[32] = acc;
+    }
+    __syncthreads();
+    ++nsub;
+    return scratch[32];
   }
   // One value per thread -> the team sum in every thread of every CTA, as
   // reduce<T, 1> but in ONE global round trip for cooperative grids: the
