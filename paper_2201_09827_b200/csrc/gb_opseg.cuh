@@ -90,6 +90,19 @@ GB_DEVICE double f2d(TF x) {
     return (double)x;
   }
 }
+// the same conversion (exact) on the integer pipe: F2F.F64.F32 issues at a
+// quarter of the FMA rate and would cap a sweep that converts every factor
+// entry once
+template <class TF>
+GB_DEVICE double f2d_fast(TF x) {
+  if constexpr (sizeof(TF) == 2) {
+    return h2d_int(__half2float(x));
+  } else if constexpr (sizeof(TF) == 4) {
+    return f2d_int(x);
+  } else {
+    return (double)x;
+  }
+}
 
 // 8 consecutive factor entries (16 B of fp16, 32 B of fp32, 64 B of fp64)
 template <class TF>
@@ -809,8 +822,8 @@ __device__ __noinline__ void sweep_bsp(Team& t, int n, int NB, const TF* __restr
 #pragma unroll
             for (int j = 0; j < VW; ++j) {
               const double y = vs[v * VW + j];
-              a[j & 3] = __fma_rn(f2d<TF>(e0[j]), y, a[j & 3]);
-              b[j & 3] = __fma_rn(f2d<TF>(e1[j]), y, b[j & 3]);
+              a[j & 3] = __fma_rn(f2d_fast<TF>(e0[j]), y, a[j & 3]);
+              b[j & 3] = __fma_rn(f2d_fast<TF>(e1[j]), y, b[j & 3]);
             }
           }
         }
@@ -893,8 +906,8 @@ GB_DEVICE void bsp_update_rows(const TF* __restrict__ LU, size_t ldf, int c0, in
 #pragma unroll
         for (int j = 0; j < VW; ++j) {
           const double y = vs[v * VW + j];
-          a[j & 3] = __fma_rn(f2d<TF>(e0[j]), y, a[j & 3]);
-          b[j & 3] = __fma_rn(f2d<TF>(e1[j]), y, b[j & 3]);
+          a[j & 3] = __fma_rn(f2d_fast<TF>(e0[j]), y, a[j & 3]);
+          b[j & 3] = __fma_rn(f2d_fast<TF>(e1[j]), y, b[j & 3]);
         }
       }
     }
@@ -1173,12 +1186,30 @@ __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A,
       const float2* ch = reinterpret_cast<const float2*>(ring + (size_t)st * GCH);
       const double2* vv = reinterpret_cast<const double2*>(vs + e0);
       const int np = (ne + 1) / 2;  // v is zero-padded past n
+      // a full chunk is 8 pairs per thread: all 16 shared-memory loads are
+      // issued before the first conversion (the warp's only latency hiding
+      // at 8 warps per SM is its own ILP)
+      if (np == EPC / 2) {
+        float2 a2[8];
+        double2 w2[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a2[u] = ch[threadIdx.x + u * NT];
+          w2[u] = vv[threadIdx.x + u * NT];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc0 = __fma_rn(kNormal ? f2d_normal(a2[u].x) : f2d_int(a2[u].x), w2[u].x, acc0);
+          acc1 = __fma_rn(kNormal ? f2d_normal(a2[u].y) : f2d_int(a2[u].y), w2[u].y, acc1);
+        }
+      } else {
 #pragma unroll 4
-      for (int q = threadIdx.x; q < np; q += NT) {
-        const float2 a2 = ch[q];
-        const double2 w2 = vv[q];
-        acc0 = __fma_rn(kNormal ? f2d_normal(a2.x) : f2d_int(a2.x), w2.x, acc0);
-        acc1 = __fma_rn(kNormal ? f2d_normal(a2.y) : f2d_int(a2.y), w2.y, acc1);
+        for (int q = threadIdx.x; q < np; q += NT) {
+          const float2 a2 = ch[q];
+          const double2 w2 = vv[q];
+          acc0 = __fma_rn(kNormal ? f2d_normal(a2.x) : f2d_int(a2.x), w2.x, acc0);
+          acc1 = __fma_rn(kNormal ? f2d_normal(a2.y) : f2d_int(a2.y), w2.y, acc1);
+        }
       }
     } else {
       const double* ch = reinterpret_cast<const double*>(ring + (size_t)st * GCH);
