@@ -702,6 +702,9 @@ def main():
     ap.add_argument("--budget-s", type=float, default=900.0,
                     help="wall-clock budget of the whole invocation; timed solves stop when the next one "
                          "would not fit (at least one is always timed)")
+    ap.add_argument("--profile-cycles", type=int, default=0,
+                    help="profiling only (ncu launch lists): cap the inner solver of the TIMED solves at this "
+                         "many cycles; the printed line is then not a bench value and says so")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel cfg4/cfg5 rooflines")
@@ -772,7 +775,7 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for r in runs:
-                r.solve_device()
+                r.solve_device(max_cycles=args.profile_cycles or None)
             e1.record(stream)
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -891,6 +894,8 @@ def main():
         "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded inputs, SURVEY §8(d); no dataset)",
         "steps_requested": args.steps,
+        **({"not_a_bench_value": f"timed solves truncated at {args.profile_cycles} cycles (--profile-cycles)"}
+           if args.profile_cycles else {}),
         "config": {"workload": workload_desc, "l2": "flushed between steps (512 MiB write)",
                    "parallelism": f"replicas x{world}" if specs[0].batch == 1 else f"shards x{world}",
                    "time_to_solution_ms": total_ms / steps_done / len(specs) if specs[0].batch == 1 else None,

@@ -1014,60 +1014,6 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
           z = r * rs;
           q = q * rp;
           r = r * rp;
-          // row and column updates with every load of a lane issued before
-          // its first store (elements are independent; the per-element
-          // operation order is unchanged): at p <= 256 a lane owns <= 8
-          // columns (rows), and the serial load -> fma -> store chain per
-          // element was half of a bulge step
-          if (nn <= 256) {
-            double h0[8], h1[8], h2[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = k + lane + 32 * u;
-              if (j < nn) {
-                h0[u] = HH(k, j);
-                h1[u] = HH(k + 1, j);
-                h2[u] = notlast ? HH(k + 2, j) : 0.0;
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = k + lane + 32 * u;
-              if (j < nn) {
-                double pp = h0[u] + q * h1[u];
-                if (notlast) {
-                  pp = pp + r * h2[u];
-                  HH(k + 2, j) = h2[u] - pp * z;
-                }
-                HH(k, j) = h0[u] - pp * x;
-                HH(k + 1, j) = h1[u] - pp * y;
-              }
-            }
-            __syncwarp();
-            const int iend = min(n, k + 3);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int i = lane + 32 * u;
-              if (i <= iend) {
-                h0[u] = HH(i, k);
-                h1[u] = HH(i, k + 1);
-                h2[u] = notlast ? HH(i, k + 2) : 0.0;
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int i = lane + 32 * u;
-              if (i <= iend) {
-                double pp = x * h0[u] + y * h1[u];
-                if (notlast) {
-                  pp = pp + z * h2[u];
-                  HH(i, k + 2) = h2[u] - pp * r;
-                }
-                HH(i, k) = h0[u] - pp;
-                HH(i, k + 1) = h1[u] - pp * q;
-              }
-            }
-          } else {
           for (int j = k + lane; j < nn; j += 32) {
             double pp = HH(k, j) + q * HH(k + 1, j);
             if (notlast) {
@@ -1087,7 +1033,6 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
             }
             HH(i, k) = HH(i, k) - pp;
             HH(i, k + 1) = HH(i, k + 1) - pp * q;
-          }
           }
           zpush(0, k, notlast ? 1 : 0, x, y, z, q, r);
           __syncwarp();  // column update visible to the next step's scalars
