@@ -699,7 +699,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
-    ap.add_argument("--budget-s", type=float, default=900.0,
+    ap.add_argument("--budget-s", type=float, default=640.0,
                     help="wall-clock budget of the whole invocation; timed solves stop when the next one "
                          "would not fit (at least one is always timed)")
     ap.add_argument("--profile-cycles", type=int, default=0,

@@ -800,6 +800,64 @@ __device__ __noinline__ void sweep_bsp(Team& t, int n, int NB, const TF* __restr
     constexpr int VW = 16 / sizeof(TF);
     const int nv = (m + VW - 1) / VW;
     // two rows per warp pass, up to 8 x 16 B per row and lane in flight
+    if (nv <= 32 * 8) {
+      // one batch per row pair: software-pipelined, the next pair's 16 loads
+      // per lane are issued before this pair's conversions and FMAs (a pass
+      // is ~1.8 us of issue time on top of ~2 us of DRAM latency otherwise)
+      uint4 q0[8], q1[8];
+      auto load_pair = [&](int r, uint4 (&x0)[8], uint4 (&x1)[8]) {
+        const bool two = r + W < hi;
+        const uint4* f0 = reinterpret_cast<const uint4*>(LU + (size_t)r * ldf + r0);
+        const uint4* f1 = reinterpret_cast<const uint4*>(LU + (size_t)(two ? r + W : r) * ldf + r0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int v = lane + 32 * u;
+          x0[u] = v < nv ? __ldg(f0 + v) : make_uint4(0, 0, 0, 0);
+          x1[u] = (v < nv && two) ? __ldg(f1 + v) : make_uint4(0, 0, 0, 0);
+        }
+      };
+      int r = lo + gw;
+      if (r < hi) load_pair(r, q0, q1);
+      for (; r < hi; r += 2 * W) {
+        const bool two = r + W < hi;
+        uint4 n0[8], n1[8];
+        const bool more = r + 2 * W < hi;
+        if (more) load_pair(r + 2 * W, n0, n1);
+        double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int v = lane + 32 * u;
+          if (v < nv) {
+            const TF* e0 = reinterpret_cast<const TF*>(&q0[u]);
+            const TF* e1 = reinterpret_cast<const TF*>(&q1[u]);
+#pragma unroll
+            for (int j = 0; j < VW; ++j) {
+              const double y = vs[v * VW + j];
+              a[j & 3] = __fma_rn(f2d<TF>(e0[j]), y, a[j & 3]);
+              b[j & 3] = __fma_rn(f2d<TF>(e1[j]), y, b[j & 3]);
+            }
+          }
+        }
+        double s0 = __dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3]));
+        double s1 = __dadd_rn(__dadd_rn(b[0], b[1]), __dadd_rn(b[2], b[3]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 = __dadd_rn(s0, __shfl_xor_sync(0xffffffffu, s0, o));
+          s1 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+        }
+        if (lane == 0) {
+          ybuf[r] = __dsub_rn(ybuf[r], s0);
+          if (two) ybuf[r + W] = __dsub_rn(ybuf[r + W], s1);
+        }
+        if (more) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            q0[u] = n0[u];
+            q1[u] = n1[u];
+          }
+        }
+      }
+    } else
     for (int r = lo + gw; r < hi; r += 2 * W) {
       const bool two = r + W < hi;
       const uint4* f0 = reinterpret_cast<const uint4*>(LU + (size_t)r * ldf + r0);
@@ -822,8 +880,8 @@ __device__ __noinline__ void sweep_bsp(Team& t, int n, int NB, const TF* __restr
 #pragma unroll
             for (int j = 0; j < VW; ++j) {
               const double y = vs[v * VW + j];
-              a[j & 3] = __fma_rn(f2d_fast<TF>(e0[j]), y, a[j & 3]);
-              b[j & 3] = __fma_rn(f2d_fast<TF>(e1[j]), y, b[j & 3]);
+              a[j & 3] = __fma_rn(f2d<TF>(e0[j]), y, a[j & 3]);
+              b[j & 3] = __fma_rn(f2d<TF>(e1[j]), y, b[j & 3]);
             }
           }
         }
@@ -906,8 +964,8 @@ GB_DEVICE void bsp_update_rows(const TF* __restrict__ LU, size_t ldf, int c0, in
 #pragma unroll
         for (int j = 0; j < VW; ++j) {
           const double y = vs[v * VW + j];
-          a[j & 3] = __fma_rn(f2d_fast<TF>(e0[j]), y, a[j & 3]);
-          b[j & 3] = __fma_rn(f2d_fast<TF>(e1[j]), y, b[j & 3]);
+          a[j & 3] = __fma_rn(f2d<TF>(e0[j]), y, a[j & 3]);
+          b[j & 3] = __fma_rn(f2d<TF>(e1[j]), y, b[j & 3]);
         }
       }
     }
