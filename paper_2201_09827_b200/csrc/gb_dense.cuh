@@ -632,8 +632,18 @@ __host__ __device__ inline int hqr_z_warps(int p, int nwarps_cta) {
   const int have = nwarps_cta - 1;
   return want < 1 ? 1 : (want < have ? want : have);
 }
-static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
-                                double* ort, double* hp = nullptr, int nz = 1, bool reduced = false) {
+struct ZShared {
+  ZRec ring[kZRing];
+  volatile int head, done;
+  volatile int tail[8];
+};
+static __device__ __noinline__ ZShared& zshared() {
+  __shared__ ZShared z;
+  return z;
+}
+template <bool kPacked>
+static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
+                                  double* ort, double* hp, int nz, bool reduced) {
   // called by threads 0 .. 32 (1 + nz) - 1: warp 0 runs orthes + the QR
   // iteration, warps 1 .. nz apply the Schur-vector updates it pushes.  Z
   // warp w owns the rows i = w - 1 + nz * t (t = 0, 1, ...) strided by lane:
@@ -642,9 +652,11 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
   // keeps Z(i, k .. k+2) of its row in registers, shifts them by one column
   // per record (one store, one load issued a record ahead) and only falls
   // back to plain loads when the sweep restarts.
-  __shared__ ZRec zring[kZRing];
-  __shared__ volatile int s_head, s_done;
-  __shared__ volatile int s_tail[8];
+  ZShared& zs = zshared();  // one instance for both storage variants
+  ZRec* const zring = zs.ring;
+  volatile int& s_head = zs.head;
+  volatile int& s_done = zs.done;
+  volatile int* const s_tail = zs.tail;
   const int lane = threadIdx.x & 31;
   const int low_ = 0, high_ = p - 1;
   const int zbar = 32 * (1 + nz);
@@ -802,7 +814,7 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
   __syncwarp();
   asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // start the Z warps
 
-  const bool packed = hp != nullptr;
+  constexpr bool packed = kPacked;  // compile-time: the accessor sits in the hottest loop of cfg2
   double* const hbase = packed ? hp : H;
   auto HH = [&](int i, int j) -> double& { return hbase[(packed ? ((j * (j + 7)) >> 1) : j * ld) + i]; };
   if (packed) {
@@ -1050,6 +1062,12 @@ static __device__ __noinline__ bool warp_hqr(double* H, int ld, int p, double* Z
   }
   zfinish();
   return true;
+}
+
+static __device__ __forceinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
+                                               double* ort, double* hp = nullptr, int nz = 1, bool reduced = false) {
+  return hp != nullptr ? warp_hqr_t<true>(H, ld, p, Z, ldz, wr, wi, ort, hp, nz, reduced)
+                       : warp_hqr_t<false>(H, ld, p, Z, ldz, wr, wi, ort, hp, nz, reduced);
 }
 
 GB_DEVICE void cdiv(double xr, double xi, double yr, double yi, double& cr, double& ci) {

@@ -366,9 +366,11 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
     // slots are polled in a fraction of the time 148 take.  The other CTAs
     // wait at the barrier below; the h column is broadcast through colbuf.
     bool sub_done = false;
-    if constexpr (Team::kGrid) {
+    // (cooperative-grid team type only: the cluster kernel must not carry this code, its
+    // register budget is what the cfg2 step time hangs on)
+    if constexpr (Team::kGrid && Team::kTB == kTrsvB) {
       int T = 0;
-      if (!t.clu && t.spart == nullptr && t.size() > 32 && j + 2 <= kColBuf) T = min(32, (n + 1023) / 1024);
+      if (!t.clu && t.spart == nullptr && t.size() > 32 && j + 2 <= kColBuf && n <= 32 * 1024) T = (n + 1023) / 1024;
       if (T > 0) {
       sub_done = true;
       constexpr int QW = 4;
@@ -443,7 +445,10 @@ __device__ CycleOut arnoldi_cycle(Team& t, Krylov<TW, TA, TF, MV>& K, TrsvSync& 
           vn[q] = vc[q];
           vc[q] = (r < hi && i < j) ? K.V[(size_t)(i + 1) * ldv + r] : TW(0);
         }
-        a[0] = t.template reduce1<typename F::Acc>(a[0], reinterpret_cast<typename F::Acc*>(red));
+        if constexpr (Team::kGrid && Team::kTB == kTrsvB)
+          a[0] = t.template reduce1<typename F::Acc>(a[0], reinterpret_cast<typename F::Acc*>(red));
+        else
+          t.template reduce<typename F::Acc, 1>(a, reinterpret_cast<typename F::Acc*>(red));
         hprev = (double)a[0];
         if (threadIdx.x == 0) col[i] = hprev;
       }
