@@ -627,9 +627,9 @@ static __device__ __noinline__ void blk_orthes(double* H, int ld, int p, double*
 }
 
 // number of Schur-vector warps warp_hqr wants next to the QR warp
-__host__ __device__ inline int hqr_z_warps(int p, int nwarps_cta) {
+__host__ __device__ inline int hqr_z_warps(int p, int nwarps_cta, int nq = 1) {
   const int want = (p + 31) / 32;
-  const int have = nwarps_cta - 1;
+  const int have = nwarps_cta - nq;
   return want < 1 ? 1 : (want < have ? want : have);
 }
 struct ZShared {
@@ -643,7 +643,7 @@ static __device__ __noinline__ ZShared& zshared() {
 }
 template <bool kPacked>
 static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
-                                  double* ort, double* hp, int nz, bool reduced) {
+                                  double* ort, double* hp, int nz, bool reduced, int nq) {
   // called by threads 0 .. 32 (1 + nz) - 1: warp 0 runs orthes + the QR
   // iteration, warps 1 .. nz apply the Schur-vector updates it pushes.  Z
   // warp w owns the rows i = w - 1 + nz * t (t = 0, 1, ...) strided by lane:
@@ -659,9 +659,17 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
   volatile int* const s_tail = zs.tail;
   const int lane = threadIdx.x & 31;
   const int low_ = 0, high_ = p - 1;
-  const int zbar = 32 * (1 + nz);
-  if ((threadIdx.x >> 5) >= 1) {
-    const int zw = (threadIdx.x >> 5) - 1;
+  // nq QR warps (1, or 4 for the large eigenproblems: the row / column updates of a bulge
+  // step are split over 128 threads, every thread keeps the scalars redundantly and the
+  // warps meet at a named barrier wherever the one-warp version has a __syncwarp)
+  const int zbar = 32 * (nq + nz);
+  const int qt = threadIdx.x, qn = 32 * nq;
+  auto qsync = [&]() {
+    if (nq == 1) __syncwarp();
+    else asm volatile("bar.sync 3, %0;" ::"r"(qn) : "memory");
+  };
+  if ((int)(threadIdx.x >> 5) >= nq) {
+    const int zw = (threadIdx.x >> 5) - nq;
     asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // Z initialised, ring reset
     int tail = 0;
     const int rows_per_pass = 32 * nz;
@@ -712,7 +720,7 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
     s_head = zh;
   };
   auto zpush = [&](int type, int k, int nl, double a0, double a1, double a2, double a3, double a4) {
-    if (lane == 0) {
+    if (qt == 0) {
       if (zh - zt >= kZRing) {
         zpublish();
         for (;;) {
@@ -736,7 +744,7 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
     }
   };
   auto zfinish = [&]() {
-    if (lane == 0) {
+    if (qt == 0) {
       zpublish();
       __threadfence_block();
       s_done = 1;
@@ -806,30 +814,30 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
     int i = e % nn, j = e / nn;
     if (i > j + 1) H[IX(i, j, ld)] = 0.0;
   }
-  if (lane == 0) {
+  if (qt == 0) {
     s_head = 0;
     for (int w = 0; w < 8; ++w) s_tail[w] = 0;
     s_done = 0;
   }
-  __syncwarp();
+  qsync();
   asm volatile("bar.sync 1, %0;" ::"r"(zbar) : "memory");  // start the Z warps
 
   constexpr bool packed = kPacked;  // compile-time: the accessor sits in the hottest loop of cfg2
   double* const hbase = packed ? hp : H;
   auto HH = [&](int i, int j) -> double& { return hbase[(packed ? ((j * (j + 7)) >> 1) : j * ld) + i]; };
   if (packed) {
-    for (int e = lane; e < p * p; e += 32) {
+    for (int e = qt; e < p * p; e += qn) {
       const int i = e % p, j = e / p;
       if (i <= j + 3) HH(i, j) = H[IX(i, j, ld)];
     }
-    __syncwarp();
+    qsync();
   }
   // --- hqr2: Francis double-shift QR with accumulation ---
   int n = nn - 1;
   const double eps = kEps52;
   double exshift = 0.0, p_ = 0, q = 0, r = 0, s = 0, z = 0, t, w, x, y;
   double norm = 0.0;
-  for (int i = lane; i < nn; i += 32)
+  for (int i = lane; i < nn; i += 32)  // every QR warp sums the whole matrix (same order, same value)
     for (int j = max(i - 1, 0); j < nn; ++j) norm += fabs(HH(i, j));
   norm = warp_sum(norm);
   int iter = 0, total = 0;
@@ -853,13 +861,13 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
       }
     }
     if (l == n) {
-      __syncwarp();
-      if (lane == 0) {
+      qsync();
+      if (qt == 0) {
         HH(n, n) = HH(n, n) + exshift;
         wr[n] = HH(n, n);
         wi[n] = 0.0;
       }
-      __syncwarp();
+      qsync();
       n--;
       iter = 0;
     } else if (l == n - 1) {
@@ -869,18 +877,18 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
       z = sqrt(fabs(q));
       double hnn = HH(n, n) + exshift;
       double hn1 = HH(n - 1, n - 1) + exshift;
-      __syncwarp();
-      if (lane == 0) {
+      qsync();
+      if (qt == 0) {
         HH(n, n) = hnn;
         HH(n - 1, n - 1) = hn1;
       }
-      __syncwarp();
+      qsync();
       x = hnn;
       if (q >= 0) {
         z = (p_ >= 0) ? p_ + z : p_ - z;
         double d1 = x + z, d2 = d1;
         if (z != 0.0) d2 = x - w / z;
-        if (lane == 0) {
+        if (qt == 0) {
           wr[n - 1] = d1;
           wr[n] = d2;
           wi[n - 1] = 0.0;
@@ -893,28 +901,28 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
         r = sqrt(p_ * p_ + q * q);
         p_ = p_ / r;
         q = q / r;
-        __syncwarp();
-        for (int j = n - 1 + lane; j < nn; j += 32) {
+        qsync();
+        for (int j = n - 1 + qt; j < nn; j += qn) {
           double zz = HH(n - 1, j);
           HH(n - 1, j) = q * zz + p_ * HH(n, j);
           HH(n, j) = q * HH(n, j) - p_ * zz;
         }
-        __syncwarp();
-        for (int i = lane; i <= n; i += 32) {
+        qsync();
+        for (int i = qt; i <= n; i += qn) {
           double zz = HH(i, n - 1);
           HH(i, n - 1) = q * zz + p_ * HH(i, n);
           HH(i, n) = q * HH(i, n) - p_ * zz;
         }
         zpush(1, n, 0, p_, 0.0, 0.0, q, 0.0);
-        __syncwarp();
+        qsync();
       } else {
-        if (lane == 0) {
+        if (qt == 0) {
           wr[n - 1] = x + p_;
           wr[n] = x + p_;
           wi[n - 1] = z;
           wi[n] = -z;
         }
-        __syncwarp();
+        qsync();
       }
       n = n - 2;
       iter = 0;
@@ -928,9 +936,9 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
       }
       if (iter == 10) {
         exshift += x;
-        __syncwarp();
-        for (int i = low + lane; i <= n; i += 32) HH(i, i) -= x;
-        __syncwarp();
+        qsync();
+        for (int i = low + qt; i <= n; i += qn) HH(i, i) -= x;
+        qsync();
         s = fabs(HH(n, n - 1)) + fabs(HH(n - 1, n - 2));
         x = y = 0.75 * s;
         w = -0.4375 * s * s;
@@ -942,9 +950,9 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
           s = sqrt(s);
           if (y < x) s = -s;
           s = x - w / ((y - x) / 2.0 + s);
-          __syncwarp();
-          for (int i = low + lane; i <= n; i += 32) HH(i, i) -= s;
-          __syncwarp();
+          qsync();
+          for (int i = low + qt; i <= n; i += qn) HH(i, i) -= s;
+          qsync();
           exshift += s;
           x = y = w = 0.964;
         }
@@ -991,12 +999,12 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
       p_ = p_ / s;
       q = q / s;
       r = r / s;
-      __syncwarp();
-      for (int i = m + 2 + lane; i <= n; i += 32) {
+      qsync();
+      for (int i = m + 2 + qt; i <= n; i += qn) {
         HH(i, i - 2) = 0.0;
         if (i > m + 2) HH(i, i - 3) = 0.0;
       }
-      __syncwarp();
+      qsync();
       for (int k = m; k <= n - 1; ++k) {
         bool notlast = (k != n - 1);
         if (k != m) {
@@ -1013,12 +1021,12 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
         s = sqrt(p_ * p_ + q * q + r * r);
         if (p_ < 0) s = -s;
         if (s != 0) {
-          __syncwarp();
-          if (lane == 0) {
+          qsync();
+          if (qt == 0) {
             if (k != m) HH(k, k - 1) = -s * x;
             else if (l != m) HH(k, k - 1) = -HH(k, k - 1);
           }
-          __syncwarp();
+          qsync();
           p_ = p_ + s;
           const double rs = 1.0 / s, rp = 1.0 / p_;
           x = p_ * rs;
@@ -1026,7 +1034,7 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
           z = r * rs;
           q = q * rp;
           r = r * rp;
-          for (int j = k + lane; j < nn; j += 32) {
+          for (int j = k + qt; j < nn; j += qn) {
             double pp = HH(k, j) + q * HH(k + 1, j);
             if (notlast) {
               pp = pp + r * HH(k + 2, j);
@@ -1035,9 +1043,9 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
             HH(k, j) = HH(k, j) - pp * x;
             HH(k + 1, j) = HH(k + 1, j) - pp * y;
           }
-          __syncwarp();
+          qsync();
           const int iend = min(n, k + 3);
-          for (int i = lane; i <= iend; i += 32) {
+          for (int i = qt; i <= iend; i += qn) {
             double pp = x * HH(i, k) + y * HH(i, k + 1);
             if (notlast) {
               pp = pp + z * HH(i, k + 2);
@@ -1047,27 +1055,28 @@ static __device__ __noinline__ bool warp_hqr_t(double* H, int ld, int p, double*
             HH(i, k + 1) = HH(i, k + 1) - pp * q;
           }
           zpush(0, k, notlast ? 1 : 0, x, y, z, q, r);
-          __syncwarp();  // column update visible to the next step's scalars
+          qsync();  // column update visible to the next step's scalars
         }
       }
     }
   }
-  __syncwarp();
+  qsync();
   if (packed) {
-    for (int e = lane; e < p * p; e += 32) {
+    for (int e = qt; e < p * p; e += qn) {
       const int i = e % p, j = e / p;
       if (i <= j + 1) H[IX(i, j, ld)] = HH(i, j);
     }
-    __syncwarp();
+    qsync();
   }
   zfinish();
   return true;
 }
 
 static __device__ __forceinline__ bool warp_hqr(double* H, int ld, int p, double* Z, int ldz, double* wr, double* wi,
-                                               double* ort, double* hp = nullptr, int nz = 1, bool reduced = false) {
-  return hp != nullptr ? warp_hqr_t<true>(H, ld, p, Z, ldz, wr, wi, ort, hp, nz, reduced)
-                       : warp_hqr_t<false>(H, ld, p, Z, ldz, wr, wi, ort, hp, nz, reduced);
+                                               double* ort, double* hp = nullptr, int nz = 1, bool reduced = false,
+                                               int nq = 1) {
+  return hp != nullptr ? warp_hqr_t<true>(H, ld, p, Z, ldz, wr, wi, ort, hp, nz, reduced, nq)
+                       : warp_hqr_t<false>(H, ld, p, Z, ldz, wr, wi, ort, hp, nz, reduced, nq);
 }
 
 GB_DEVICE void cdiv(double xr, double xi, double yr, double yi, double& cr, double& ci) {

@@ -595,14 +595,15 @@ static __device__ __noinline__ int leader_ritz_basis(double* Mx, int p, int kreq
     if (!isfinite(Mx[e])) s_ok = 0;
   __syncthreads();
   if (!s_ok) return -1;
-  const int nz = hqr_z_warps(p, (int)(blockDim.x >> 5));
+  const int nq = (p >= 128 && blockDim.x >= 256) ? 4 : 1;  // QR warps (reduced problems only, see below)
+  const int nz = hqr_z_warps(p, (int)(blockDim.x >> 5), nq);
   // large problems (cfg5: p = 200): Hessenberg form + accumulated transformation by the whole
   // CTA; small ones (cfg2: p = 50, in shared memory) stay on the QR warp, where the CTA
   // barriers would cost more than they save.  Same arithmetic either way.
   const bool wide = p >= 128;
   if (wide) blk_orthes(Mx, p, p, Z, p, ort);
-  if ((int)threadIdx.x < 32 * (1 + nz)) {  // warp 0: QR iteration, warps 1 .. nz: Schur-vector updates
-    bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort, hp, nz, wide);
+  if ((int)threadIdx.x < 32 * (nq + nz)) {  // warps 0 .. nq-1: QR iteration, then nz warps of Schur-vector updates
+    bool ok = warp_hqr(Mx, p, p, Z, p, wr, wi, ort, hp, nz, wide, nq);
     if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
   }
   __syncthreads();

@@ -203,10 +203,7 @@ __host__ __device__ constexpr size_t sweep_smem() {
 // ring of GCH-byte stages filling the rest of the budget (<= GNS_MAX)
 constexpr int GCH = 16 * 1024;  // bytes per stage
 constexpr int GNS_MAX = 8;
-constexpr int GPW = 8192;  // columns per GEMV pass (v staged as fp64: 64 KB)
-__host__ __device__ constexpr size_t gemv_vbytes(int n) {
-  return ((size_t)(n < GPW ? n : GPW) * 8 + 127) & ~(size_t)127;
-}
+__host__ __device__ constexpr size_t gemv_vbytes(int n) { return ((size_t)n * 8 + 127) & ~(size_t)127; }
 __host__ __device__ constexpr int gemv_stages(int n, size_t budget) {
   return (int)((budget - gemv_vbytes(n) - 512 - 4096) / GCH) < GNS_MAX
              ? (int)((budget - gemv_vbytes(n) - 512 - 4096) / GCH)
@@ -1112,8 +1109,7 @@ __device__ __noinline__ void gemv_ldg(Team& t, int n, const TA* __restrict__ A, 
                                       void* smem_raw) {
   constexpr int VW = 16 / sizeof(TA);
   double* vs = reinterpret_cast<double*>(smem_raw);
-  // (measurement variant, tools/micro/opseg.cu: stages ALL of v; the caller sizes the shared memory for it)
-  for (int j = threadIdx.x; j < (int)((((size_t)n * 8 + 127) & ~(size_t)127) / 8); j += NT) vs[j] = j < n ? (double)v[j] : 0.0;
+  for (int j = threadIdx.x; j < (int)(gemv_vbytes(n) / 8); j += NT) vs[j] = j < n ? (double)v[j] : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int W = t.size() * (NT / 32);
@@ -1199,11 +1195,6 @@ template <class TA, class TV, bool kNormal, class Team>
 __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A, size_t lda,
                                        const int* __restrict__ perm, const TV* __restrict__ v, double* out,
                                        void* smem_raw, int NS, const PhaseLog lg = PhaseLog{nullptr, 0, nullptr}) {
-  // Column passes of at most GPW columns: v is staged as fp64 for one pass
-  // (64 KB) and the rest of the budget is ring stages -- with all of v
-  // resident at n = 16384 (128 KB) only 4 stages fit and the copies in flight
-  // (the consumer re-arms a stage after a CTA-wide barrier) cap the stream at
-  // ~3.8 TB/s.  A row's result is the sum over the passes, added in pass order.
   constexpr int EPC = GCH / sizeof(TA);  // elements per chunk
   double* vs = reinterpret_cast<double*>(smem_raw);
   unsigned char* ring = reinterpret_cast<unsigned char*>(smem_raw) + gemv_vbytes(n);
@@ -1213,116 +1204,111 @@ __device__ __noinline__ void gemv_perm(Team& t, int n, const TA* __restrict__ A,
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int G = t.size(), r = t.rank();
   const int nrows = min(GROWS_MAX, n > r ? (n - r + G - 1) / G : 0);  // rows r, r + G, ...
+  const size_t rowbytes = ((size_t)n * sizeof(TA) + 15) & ~(size_t)15;
+  const int cpr = (int)((rowbytes + GCH - 1) / GCH);  // chunks per row
+  const int total = nrows * cpr;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(full + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < n; j += NT) vs[j] = (double)v[j];  // once per apply
+  for (int j = n + threadIdx.x; j < (int)(gemv_vbytes(n) / 8); j += NT) vs[j] = 0.0;
   for (int i = threadIdx.x; i < nrows; i += NT) rows[i] = perm[r + i * G];
-  const int npass = (n + GPW - 1) / GPW;
-  for (int pass = 0; pass < npass; ++pass) {
-    const int c0 = pass * GPW, nc = min(GPW, n - c0);
-    const size_t rowbytes = ((size_t)nc * sizeof(TA) + 15) & ~(size_t)15;
-    const int cpr = (int)((rowbytes + GCH - 1) / GCH);  // chunks per row
-    const int total = nrows * cpr;
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < NS; ++i) mbar_init(full + i, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int j = threadIdx.x; j < (int)(gemv_vbytes(n) / 8); j += NT) vs[j] = j < nc ? (double)v[c0 + j] : 0.0;
-    __syncthreads();
-    mark(lg, 14);
-    // producer state (thread 0): next chunk to issue as (row, chunk-in-row)
-    int pr = 0, pc = 0, pn = 0;
-    auto issue_next = [&]() {
-      const size_t off = (size_t)pc * GCH;
-      const unsigned bytes = (unsigned)min((size_t)GCH, rowbytes - off);
-      unsigned long long* bar = full + (pn % NS);
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(ring + (size_t)(pn % NS) * GCH,
-               reinterpret_cast<const unsigned char*>(A + (size_t)rows[pr] * lda + c0) + off, bytes, bar);
-      ++pn;
-      if (++pc == cpr) pc = 0, ++pr;
-    };
-    if (threadIdx.x == 0) {
-      fence_async_smem();  // earlier generic-proxy accesses of the ring before the async writes
-      while (pn < min(NS, total)) issue_next();
-    }
-    double acc0 = 0.0, acc1 = 0.0;
-    int ri = 0, ci = 0, st = 0;
-    unsigned ph = 0;
-    for (int c = 0; c < total; ++c) {
-      mbar_wait(full + st, ph);
-      const int e0 = ci * EPC;
-      const int ne = min(EPC, nc - e0);
-      if constexpr (sizeof(TA) == 4) {
-        // element pairs: 8 B of A and 16 B of v per lane, contiguous across the warp
-        const float2* ch = reinterpret_cast<const float2*>(ring + (size_t)st * GCH);
-        const double2* vv = reinterpret_cast<const double2*>(vs + e0);
-        const int np = (ne + 1) / 2;  // v is zero-padded past the pass
-        // a full chunk is 8 pairs per thread: all 16 shared-memory loads are
-        // issued before the first conversion (the warp's only latency hiding
-        // at 8 warps per SM is its own ILP)
-        if (np == EPC / 2) {
-          float2 a2[8];
-          double2 w2[8];
+  __syncthreads();
+  mark(lg, 14);
+  // producer state (thread 0): next chunk to issue as (row, chunk-in-row)
+  int pr = 0, pc = 0, pn = 0;
+  auto issue_next = [&]() {
+    const size_t off = (size_t)pc * GCH;
+    const unsigned bytes = (unsigned)min((size_t)GCH, rowbytes - off);
+    unsigned long long* bar = full + (pn % NS);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(ring + (size_t)(pn % NS) * GCH,
+             reinterpret_cast<const unsigned char*>(A + (size_t)rows[pr] * lda) + off, bytes, bar);
+    ++pn;
+    if (++pc == cpr) pc = 0, ++pr;
+  };
+  if (threadIdx.x == 0) {
+    fence_async_smem();  // earlier generic-proxy accesses of the ring before the async writes
+    while (pn < min(NS, total)) issue_next();
+  }
+  double acc0 = 0.0, acc1 = 0.0;
+  int ri = 0, ci = 0, st = 0;
+  unsigned ph = 0;
+  for (int c = 0; c < total; ++c) {
+    mbar_wait(full + st, ph);
+    const int e0 = ci * EPC;
+    const int ne = min(EPC, n - e0);
+    if constexpr (sizeof(TA) == 4) {
+      // element pairs: 8 B of A and 16 B of v per lane, contiguous across the warp
+      const float2* ch = reinterpret_cast<const float2*>(ring + (size_t)st * GCH);
+      const double2* vv = reinterpret_cast<const double2*>(vs + e0);
+      const int np = (ne + 1) / 2;  // v is zero-padded past n
+      // a full chunk is 8 pairs per thread: all 16 shared-memory loads are
+      // issued before the first conversion (the warp's only latency hiding
+      // at 8 warps per SM is its own ILP)
+      if (np == EPC / 2) {
+        float2 a2[8];
+        double2 w2[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            a2[u] = ch[threadIdx.x + u * NT];
-            w2[u] = vv[threadIdx.x + u * NT];
-          }
+        for (int u = 0; u < 8; ++u) {
+          a2[u] = ch[threadIdx.x + u * NT];
+          w2[u] = vv[threadIdx.x + u * NT];
+        }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            acc0 = __fma_rn(kNormal ? f2d_normal(a2[u].x) : f2d_int(a2[u].x), w2[u].x, acc0);
-            acc1 = __fma_rn(kNormal ? f2d_normal(a2[u].y) : f2d_int(a2[u].y), w2[u].y, acc1);
-          }
-        } else {
-#pragma unroll 4
-          for (int q = threadIdx.x; q < np; q += NT) {
-            const float2 a2 = ch[q];
-            const double2 w2 = vv[q];
-            acc0 = __fma_rn(kNormal ? f2d_normal(a2.x) : f2d_int(a2.x), w2.x, acc0);
-            acc1 = __fma_rn(kNormal ? f2d_normal(a2.y) : f2d_int(a2.y), w2.y, acc1);
-          }
+        for (int u = 0; u < 8; ++u) {
+          acc0 = __fma_rn(kNormal ? f2d_normal(a2[u].x) : f2d_int(a2[u].x), w2[u].x, acc0);
+          acc1 = __fma_rn(kNormal ? f2d_normal(a2[u].y) : f2d_int(a2[u].y), w2[u].y, acc1);
         }
       } else {
-        const double* ch = reinterpret_cast<const double*>(ring + (size_t)st * GCH);
 #pragma unroll 4
-        for (int q = threadIdx.x; q < ne; q += NT) acc0 = __fma_rn(ch[q], vs[e0 + q], acc0);
-      }
-      __syncthreads();  // stage consumed by every thread
-      if (threadIdx.x == 0 && pn < total) {
-        fence_async_smem();
-        issue_next();
-      }
-      if (++st == NS) st = 0, ph ^= 1u;
-      if (++ci == cpr) {
-        // row done: fixed-order block reduction
-        double s = __dadd_rn(acc0, acc1);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-        if (lane == 0) red[wid] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          double z = 0.0;
-#pragma unroll
-          for (int w = 0; w < NT / 32; ++w) z = __dadd_rn(z, red[w]);
-          double* o = out + r + ri * G;
-          *o = pass == 0 ? z : __dadd_rn(*o, z);
+        for (int q = threadIdx.x; q < np; q += NT) {
+          const float2 a2 = ch[q];
+          const double2 w2 = vv[q];
+          acc0 = __fma_rn(kNormal ? f2d_normal(a2.x) : f2d_int(a2.x), w2.x, acc0);
+          acc1 = __fma_rn(kNormal ? f2d_normal(a2.y) : f2d_int(a2.y), w2.y, acc1);
         }
-        acc0 = acc1 = 0.0;
-        ci = 0;
-        ++ri;
-        mark(lg, 15);
       }
+    } else {
+      const double* ch = reinterpret_cast<const double*>(ring + (size_t)st * GCH);
+#pragma unroll 4
+      for (int q = threadIdx.x; q < ne; q += NT) acc0 = __fma_rn(ch[q], vs[e0 + q], acc0);
     }
-    __syncthreads();
-    // the ring's barriers are re-initialised by the next pass / call (the
-    // region is shared with the sweeps' staging and the leader's scratch in
-    // between): invalidate them first -- re-initialising a live mbarrier is
-    // undefined, and a stage that has completed an odd number of phases did
-    // fault the next call's first wait at n = 16384 (111 rows x 4 chunks on 5
-    // stages)
-    if (threadIdx.x == 0)
-      for (int i = 0; i < NS; ++i)
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + i)) : "memory");
-    __syncthreads();
+    __syncthreads();  // stage consumed by every thread
+    if (threadIdx.x == 0 && pn < total) {
+      fence_async_smem();
+      issue_next();
+    }
+    if (++st == NS) st = 0, ph ^= 1u;
+    if (++ci == cpr) {
+      // row done: fixed-order block reduction
+      double s = __dadd_rn(acc0, acc1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+      if (lane == 0) red[wid] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double z = 0.0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) z = __dadd_rn(z, red[w]);
+        out[r + ri * G] = z;
+      }
+      acc0 = acc1 = 0.0;
+      ci = 0;
+      ++ri;
+      mark(lg, 15);
+    }
   }
+  __syncthreads();
+  // the ring's barriers are re-initialised by the next call (the region is
+  // shared with the sweeps' staging and the leader's scratch in between):
+  // invalidate them first -- re-initialising a live mbarrier is undefined,
+  // and a stage that has completed an odd number of phases did fault the
+  // next call's first wait at n = 16384 (111 rows x 4 chunks on 5 stages)
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NS; ++i)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + i)) : "memory");
+  __syncthreads();
   mark(lg, 16);
 }
 
