@@ -1071,9 +1071,18 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
   // 2^53 / (4 p) proves the pencil regular without the SVD; otherwise (and
   // without the fast staging) the 2-norm condition number decides.
   bool need_cond2 = true;
-  int zero = fast ? blk_getrf(lu, gc, gc, piv) : -1;
-  if (fast && zero < 0) {
-    double* inv = K.fast + 2 * pp;
+  if (!fast) {
+    // large pencils (cfg5: gc = 200) run the same screen in global memory: b1 is kept in
+    // b1c, factored in place, inverted into the eig scratch; the bidiagonalisation-based
+    // cond2 (18 ms at gc = 200, against ~5 ms for the inverse) only runs if the screen fails
+    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) b1c[e] = b1[e];
+    __syncthreads();
+  }
+  int zero = blk_getrf(lu, gc, gc, piv);  // lu == b1 without the fast staging
+  bool screened = false;
+  if (zero < 0) {
+    double* inv = fast ? K.fast + 2 * pp : scr;
+    const double* b1orig = fast ? b1 : b1c;
     for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) inv[e] = (e % gc == e / gc) ? 1.0 : 0.0;
     __syncthreads();
     blk_getrs(lu, gc, gc, piv, inv, gc, gc);
@@ -1081,7 +1090,7 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
     if (threadIdx.x < 64) {
       const int lane = threadIdx.x & 31;
       // column sums: warp 0 over b1, warp 1 over the inverse
-      const double* m = threadIdx.x < 32 ? b1 : inv;
+      const double* m = threadIdx.x < 32 ? b1orig : inv;
       double best = 0.0;
       for (int c = lane; c < gc; c += 32) {
         double cs = 0.0;
@@ -1095,7 +1104,14 @@ __device__ int leader_recycle(const Team& t, Krylov<TW, TA, TF, MV>& K, int keff
     __syncthreads();
     const double c1 = s_n1[0] * s_n1[1];
     need_cond2 = !(c1 * 4.0 * gc < 1.0 / kEps53);
+    screened = !need_cond2;
     __syncthreads();
+  }
+  if (!fast && !screened) {
+    // the screen did not decide: restore b1 and take the cond2 path below unchanged
+    for (int e = threadIdx.x; e < gc * gc; e += blockDim.x) b1[e] = b1c[e];
+    __syncthreads();
+    zero = -1;
   }
   if (need_cond2) {
     double* cmat = fast ? K.fast + 2 * pp : b1c;
